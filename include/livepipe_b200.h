@@ -1,0 +1,254 @@
+/*
+ * livepipe_b200.h -- C ABI of liblivepipe_b200.so, the B200 (sm_100a) kernels
+ * behind the livepipe streaming-denoiser hot path.
+ *
+ * The reference (Python/NumPy, /root/reference/pkg/src/livepipe) has one
+ * plugin point on this path: the duck-typed denoiser object the engine calls,
+ * `ToyDenoiser.denoise_block` (denoiser.py:201-276), picked by
+ * `build_runtime` (engine.py:177-201).  The Python class
+ * `paper_2512_04677_b200.denoiser.B200Denoiser` keeps that signature and calls
+ * the entry points below through ctypes.  Every entry point takes plain
+ * pointers / sizes and an explicit cudaStream_t (passed as void*), returns 0
+ * on success or an LP_E* code (message via lp_last_error()), never throws, and
+ * allocates nothing on the hot path (all buffers come from the caller).
+ *
+ * Each entry point names the reference function it replaces.
+ */
+#ifndef LIVEPIPE_B200_H
+#define LIVEPIPE_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LP_API __attribute__((visibility("default")))
+#else
+#define LP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LP_ABI_VERSION 1
+
+/* status codes */
+#define LP_OK 0
+#define LP_EINVAL 1       /* bad argument (shape, alignment, null pointer) */
+#define LP_ECUDA 2        /* CUDA runtime / driver error */
+#define LP_EUNSUPPORTED 3 /* shape or mode this build does not handle */
+#define LP_ETIMEOUT 4     /* a stage-link wait exceeded its bound */
+#define LP_EABORT 5       /* another stage raised the pipeline abort flag */
+
+/* element types */
+#define LP_F32 0
+#define LP_BF16 1
+
+/* GEMM epilogues (what happens to acc = A.W for output element (r, c)) */
+#define LP_EPI_STORE 0      /* c = acc + bias[c]               (out dtype = args.out_dtype) */
+#define LP_EPI_RELU 1       /* c = max(acc, 0)                                             */
+#define LP_EPI_GELU 2       /* c = gelu_tanh(acc)                                          */
+#define LP_EPI_RESID 3      /* h[r,c] = h[r,c] + gate[c] * acc   (h fp32; gate NULL => 1)  */
+#define LP_EPI_QKV 4        /* columns [0,d)->q, [d,2d)->k ring slot, [2d,3d)->v ring slot,
+                               with optional per-head RMSNorm and rotary embedding         */
+
+#define LP_MAX_SEG 66  /* sink + up to 64 history blocks + current block */
+#define LP_MAX_PAIRS 64
+
+/*
+ * Per-call block descriptor, resident in DEVICE memory and rewritten by the
+ * host before each forward (one small async copy), so a captured CUDA graph
+ * can replay every block of a stream.  Replaces the per-call arguments of
+ * denoise_block (denoiser.py:201-211): block index, t_index, the cache view
+ * (as KV-arena row segments: sink, history oldest->newest, current --
+ * denoiser.py:248-253), sink_rope_index (kvcache.py:86-90) and the flow
+ * step dt (latent.py:140-147).
+ */
+typedef struct lp_block_desc {
+  int32_t block_index;    /* i: temporal rotary position of every token    */
+  int32_t t_index;        /* j                                             */
+  int32_t sink_pos;       /* i + delta                                     */
+  int32_t n_seg;          /* number of KV segments (>= 2: sink, current)   */
+  int32_t cur_row;        /* arena row where this block's K/V are written  */
+  int32_t n_tokens;       /* tokens in the current block                   */
+  int32_t seg_row[LP_MAX_SEG];
+  int32_t seg_len[LP_MAX_SEG];
+  int32_t src_row[LP_MAX_SEG]; /* history noise: uncorrupted ring rows      */
+  float dt;               /* Euler step (negative)                         */
+  float sigma;            /* history-noise std (0 = off)                   */
+  uint64_t noise_key;     /* device-RNG key for history noise (perf runs)  */
+  /* temporal-axis rotary cos/sin (pairs of the t axis), fp64 angle -> fp32 */
+  float rope_cos[LP_MAX_PAIRS];
+  float rope_sin[LP_MAX_PAIRS];
+  float sink_cos[LP_MAX_PAIRS];
+  float sink_sin[LP_MAX_PAIRS];
+} lp_block_desc;
+
+/* Static rotary geometry of one model (per-head pair layout). */
+typedef struct lp_rope_geom {
+  int32_t head_dim;
+  int32_t t_pairs;        /* pairs [0, t_pairs) use the temporal position   */
+  int32_t tokens_per_frame;
+  /* pairs [t_pairs, head_dim/2) use per-token spatial tables:
+     cos/sin[(token % tokens_per_frame) * spatial_pairs + p]             */
+  int32_t spatial_pairs;
+  const float* spatial_cos;
+  const float* spatial_sin;
+} lp_rope_geom;
+
+/* ---------------------------------------------------------------- setup */
+LP_API int lp_abi_version(void);
+LP_API const char* lp_last_error(void);
+/* Select the device and resolve cuTensorMapEncodeTiled; idempotent. */
+LP_API int lp_init(int device);
+LP_API int lp_num_sms(void);
+
+/* ---------------------------------------------------------------- GEMM
+ * replaces numerics.matmul (numerics.py:50-64) at every projection site of
+ * denoise_block: QKV :240-242, O :265, FFN :266, velocity head :268.
+ *   LP_F32 : A fp32 [m,k] (lda), W fp32 [k,n] row-major (in x out, as the
+ *            reference stores it, ldw); ascending-k, separately rounded
+ *            mul/add (bit-faithful to the reference's pinned order).
+ *   LP_BF16: A bf16 [m,k], W^T bf16 [n,k] (K-major); tcgen05.mma, fp32
+ *            accumulation in TMEM, TMA-fed; k % 64 == 0, n % 16 == 0.
+ */
+typedef struct lp_qkv_epi {
+  int32_t d;              /* model dim; GEMM n == 3*d                       */
+  int32_t n_heads;
+  int32_t head_dim;
+  int32_t qk_norm;        /* per-head RMSNorm before rotation               */
+  float eps;
+  const float* g_q;       /* [d] or NULL                                    */
+  const float* g_k;
+  void* q_out;            /* [m, d] (dtype of the KV arena)                 */
+  void* k_arena;          /* this layer's K arena base ([rows, d])          */
+  void* v_arena;
+  const lp_block_desc* desc; /* device: cur_row, rope_cos/sin               */
+  lp_rope_geom geom;
+} lp_qkv_epi;
+
+typedef struct lp_gemm_args {
+  int32_t in_dtype;       /* LP_F32 | LP_BF16                               */
+  int32_t out_dtype;      /* for STORE/RELU/GELU                            */
+  int32_t epilogue;       /* LP_EPI_*                                       */
+  int32_t m, n, k;
+  int64_t lda, ldw, ldc;
+  const void* a;
+  const void* w;
+  void* c;                /* output (or fp32 residual h for LP_EPI_RESID)   */
+  const float* bias;      /* [n] or NULL (STORE only)                       */
+  const float* gate;      /* [n] or NULL (RESID only)                       */
+  const lp_qkv_epi* qkv;  /* host pointer, LP_EPI_QKV only                  */
+} lp_gemm_args;
+LP_API int lp_gemm(const lp_gemm_args* args, void* stream);
+
+/* ---------------------------------------------------------------- attention
+ * replaces the per-head loop of denoise_block (denoiser.py:246-264) and
+ * _attend_head (:152-158): softmax(q K^T / sqrt(hd)) V over the visible keys
+ * [sink | history oldest->newest | current] (segments from desc), no mask.
+ *   LP_F32 : SIMT, reference summation order (numpy pairwise row sum).
+ *   LP_BF16: tcgen05 flash attention, S/O in TMEM, fp32 online softmax.
+ */
+typedef struct lp_attn_args {
+  int32_t dtype;
+  int32_t n_q, n_heads, head_dim;
+  float scale;
+  const void* q;          /* [n_q, n_heads*hd]                              */
+  const void* k_arena;    /* layer base, rows addressed by desc segments    */
+  const void* v_arena;
+  void* out;              /* [n_q, n_heads*hd]                              */
+  const lp_block_desc* desc;
+  int32_t arena_rows;     /* rows in the arena (bounds for TMA)             */
+  int32_t n_kv_max;       /* host-known upper bound of visible keys         */
+} lp_attn_args;
+LP_API int lp_attention(const lp_attn_args* args, void* stream);
+/* SIMT reference attention for either dtype (validation tool: same math,
+   reference order; used by tests to check the tcgen05 kernel on identical
+   bf16 inputs).  Never used by the bf16 product path.                     */
+LP_API int lp_attention_simt(const lp_attn_args* args, void* stream);
+
+/* ---------------------------------------------------------------- row kernels */
+/* cond row (denoiser.py:178-185): c = a.Wa + p.Wp + tau.Wt in that order.
+   inputs fp32; tau precomputed by host (fp64 -> fp32).                     */
+LP_API int lp_cond_row(const float* audio, int audio_dim, const float* w_audio,
+                const float* prompt, int prompt_dim, const float* w_prompt,
+                const float* tau, int tau_dim, const float* w_time,
+                float* out, int d, void* stream);
+
+/* h[r, :] = x[r, :] + c  (denoiser.py:236), toy embed (no patching)        */
+LP_API int lp_add_row(const float* x, const float* c, float* h, int rows, int d, void* stream);
+
+/* out = modulate(norm(h)) cast to out_dtype.  mode: 0 = copy (toy, no norm),
+   1 = LayerNorm, 2 = LayerNorm*(1+scale)+shift.  shift/scale fp32 [d].     */
+LP_API int lp_norm_mod(const float* h, int rows, int d, int mode, float eps,
+                const float* shift, const float* scale, void* out, int out_dtype,
+                void* stream);
+
+/* Sink K/V at the block's sink position (denoiser.py:187-190, :246-249) for
+   n_layers layers in one launch: k_raw/v_raw fp32 [S, d] per layer
+   (raw_layer_stride elements apart) are the un-rotated projections of the
+   sink latent, computed once per sink content (RSFM: after the one-shot AAS
+   swap); writes (optionally per-head-RMS-normed) rotated K and V into arena
+   rows [desc->seg_row[0], +S) of every layer (arena_layer_stride apart).   */
+LP_API int lp_sink_refresh(const float* k_raw, const float* v_raw, int s_tokens, int d,
+                    int n_heads, int qk_norm, const float* g_k, float eps,
+                    const lp_block_desc* desc, const lp_rope_geom* geom,
+                    void* k_arena, void* v_arena, int arena_dtype, int n_layers,
+                    int64_t raw_layer_stride, int64_t arena_layer_stride, void* stream);
+/* out[i] = silu(x[i]) cast to out_dtype (AdaLN input, wan profile)         */
+LP_API int lp_silu(const float* x, void* out, int n, int out_dtype, void* stream);
+/* QKV post-processing for the SIMT path (the tcgen05 GEMM fuses this into its
+   epilogue): qkv fp32 [m, 3d] -> per-head RMSNorm (opt.), rotary, q -> q_out,
+   k/v -> arena rows desc->cur_row + r.                                     */
+LP_API int lp_qkv_post(const float* qkv, int m, const lp_qkv_epi* epi, int out_dtype, void* stream);
+
+/* Patchify / embed inputs and the velocity head's scatter + Euler step.
+   patchify: x frames [F, C*H*W] fp32 -> tokens [F*Hp*Wp, C*ph*pw] (dtype).  */
+LP_API int lp_patchify(const float* x, int frames, int c, int h, int w, int ph, int pw,
+                void* tokens, int out_dtype, void* stream);
+/* x_out = x + unpatchify(v_tokens) * dt   (latent.py:140-147), fp32.
+   ph == 0 => toy: tokens are frames, x_out[r,c] = x[r,c] + v[r,c]*dt.      */
+LP_API int lp_unpatchify_euler(const float* x, const float* v_tokens, int frames, int c,
+                        int h, int w, int ph, int pw, const lp_block_desc* desc,
+                        float* x_out, void* stream);
+
+/* History noise (kvcache.py:121-137) for one layer and one of K/V (kv 0/1):
+   for every history segment s in [1, n_seg-1) of desc, arena rows
+   [seg_row[s], +seg_len[s]) = arena rows [src_row[s], +seg_len[s])
+   + desc->sigma * z (the stored ring rows are never modified).  z comes from
+   `noise` (host-generated in the reference draw order,
+   [entry][kv][layer][rows][d], parity runs) or, when noise == NULL, from the
+   device Philox4x32 stream keyed by desc->noise_key (perf runs).
+   max_rows bounds the history rows (grid size).                            */
+LP_API int lp_history_noise(void* arena, int dtype, int d, const float* noise, int n_layers, int layer,
+                     int kv, const lp_block_desc* desc, int max_rows, void* stream);
+
+/* Device N(0,1) fp32 fill (perf-run weights / block noise), Philox4x32 +
+   Box-Muller keyed by (seed, stream).  scale multiplies every sample.     */
+LP_API int lp_randn(float* out, int64_t n, uint64_t seed, uint64_t stream_id, float scale,
+             void* stream);
+LP_API int lp_randn_bf16(void* out, int64_t n, uint64_t seed, uint64_t stream_id, float scale,
+                  void* stream);
+
+/* ---------------------------------------------------------------- TPP links
+ * replace _Link.send/recv (engine.py:342-388) and the one-shot sink fan-out
+ * (:417, :477-478).  A link is a ring of `capacity` payload slots plus
+ * monotone 32-bit flags in (peer-mapped) device memory:
+ *   ready[s] = sequence+1 published by the producer (release, system scope),
+ *   free[s]  = sequence+1 consumed, published by the consumer.
+ * lp_link_send copies `bytes` into slot (seq % capacity) of the consumer's
+ * receive buffer (peer pointer over NVLink, or local) after waiting for the
+ * slot to be free, then publishes ready.  lp_link_recv waits for ready and
+ * copies out.  Waits spin on the device with a bound (timeout_ns) and poll
+ * the host-mapped abort word.                                              */
+LP_API int lp_link_send(const void* src, void* dst_slot, int64_t bytes, volatile uint32_t* ready_flag,
+                 volatile const uint32_t* free_flag, uint32_t seq, int capacity,
+                 volatile const uint32_t* abort_word, uint64_t timeout_ns, void* stream);
+LP_API int lp_link_recv(const void* src_slot, void* dst, int64_t bytes, volatile const uint32_t* ready_flag,
+                 volatile uint32_t* free_flag, uint32_t seq,
+                 volatile const uint32_t* abort_word, uint64_t timeout_ns,
+                 int32_t* status_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIVEPIPE_B200_H */

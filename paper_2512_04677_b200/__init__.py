@@ -1,0 +1,34 @@
+"""paper_2512_04677_b200: B200-native streaming-denoiser hot path of Live Avatar
+(arXiv 2512.04677) -- the few-step block-causal DiT denoiser under
+Timestep-forcing Pipeline Parallelism with the Rolling Sink Frame Mechanism.
+
+Keeps the reference ``livepipe`` model/pipeline API names for this path
+(reference src/__init__.py:9-79); the compute runs in liblivepipe_b200.so
+(hand-written sm_100a kernels, C ABI in include/livepipe_b200.h).
+"""
+
+import os as _os
+
+# Stage links spin on the device; with lazy module loading a first-time kernel
+# launch can wait on a spinning waiter.  Must be set before CUDA initialises.
+_os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
+from .denoiser import (B200Denoiser, BlockCond, DenoiseOutput, KvEntry, TimestepForcingError,
+                       check_view)
+from .engine import (EngineConfig, EngineConfigError, PipelineInvariantError, RolloutResult, StageMessage,
+                     build_runtime, count_nfe, noise_block, run, run_clean_kv, run_sequential, run_tpp,
+                     StreamingPipeline)
+from .kvcache import (RollingKvCache, SinkLockedError, SinkSlot, aas_update, cache_push, corrupt_history,
+                      corruption_prng, receive_sink, rolling_rope_index)
+from .latent import (Conditions, LatentBlock, TimestepSchedule, ToyVideoCodec, flow_step, interpolate,
+                     synthetic_conditions, true_velocity)
+from .metrics import (MetricsBundle, TimelineEvent, compute_fps, compute_ttff, drift_metric,
+                      metrics_from_timeline, stage_utilization)
+from .model import (WAN_14B, WAN_1_3B, DenoiserWeights, DeviceWeights, LayerWeights, ModelProfile,
+                    build_weights, toy_profile, wan_profile)
+from .numerics import Prng, gaussian
+
+# the reference's class name for the plug-in point (engine.py:200)
+ToyDenoiser = B200Denoiser
+
+__version__ = "0.1.0"

@@ -1,0 +1,140 @@
+"""ctypes binding of liblivepipe_b200.so (include/livepipe_b200.h).
+
+The library is the only compute path: if it is missing or fails to
+initialise on a CUDA device, every op raises -- there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblivepipe_b200.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "livepipe_b200.h")
+
+LP_OK, LP_EINVAL, LP_ECUDA, LP_EUNSUPPORTED, LP_ETIMEOUT, LP_EABORT = range(6)
+LP_F32, LP_BF16 = 0, 1
+EPI_STORE, EPI_RELU, EPI_GELU, EPI_RESID, EPI_QKV = range(5)
+MAX_SEG = 66
+MAX_PAIRS = 64
+
+vp = C.c_void_p
+i32, i64, u32, u64, f32 = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_float
+fp = C.POINTER(C.c_float)
+
+
+class BlockDesc(C.Structure):
+    _fields_ = [
+        ("block_index", i32), ("t_index", i32), ("sink_pos", i32), ("n_seg", i32),
+        ("cur_row", i32), ("n_tokens", i32),
+        ("seg_row", i32 * MAX_SEG), ("seg_len", i32 * MAX_SEG), ("src_row", i32 * MAX_SEG),
+        ("dt", f32), ("sigma", f32), ("noise_key", u64),
+        ("rope_cos", f32 * MAX_PAIRS), ("rope_sin", f32 * MAX_PAIRS),
+        ("sink_cos", f32 * MAX_PAIRS), ("sink_sin", f32 * MAX_PAIRS),
+    ]
+
+
+class RopeGeom(C.Structure):
+    _fields_ = [("head_dim", i32), ("t_pairs", i32), ("tokens_per_frame", i32),
+                ("spatial_pairs", i32), ("spatial_cos", vp), ("spatial_sin", vp)]
+
+
+class QkvEpi(C.Structure):
+    _fields_ = [("d", i32), ("n_heads", i32), ("head_dim", i32), ("qk_norm", i32), ("eps", f32),
+                ("g_q", vp), ("g_k", vp), ("q_out", vp), ("k_arena", vp), ("v_arena", vp),
+                ("desc", vp), ("geom", RopeGeom)]
+
+
+class GemmArgs(C.Structure):
+    _fields_ = [("in_dtype", i32), ("out_dtype", i32), ("epilogue", i32), ("m", i32), ("n", i32),
+                ("k", i32), ("lda", i64), ("ldw", i64), ("ldc", i64), ("a", vp), ("w", vp), ("c", vp),
+                ("bias", vp), ("gate", vp), ("qkv", C.POINTER(QkvEpi))]
+
+
+class AttnArgs(C.Structure):
+    _fields_ = [("dtype", i32), ("n_q", i32), ("n_heads", i32), ("head_dim", i32), ("scale", f32),
+                ("q", vp), ("k_arena", vp), ("v_arena", vp), ("out", vp), ("desc", vp),
+                ("arena_rows", i32), ("n_kv_max", i32)]
+
+
+_SIGS = {
+    "lp_abi_version": ([], C.c_int),
+    "lp_last_error": ([], C.c_char_p),
+    "lp_init": ([C.c_int], C.c_int),
+    "lp_num_sms": ([], C.c_int),
+    "lp_gemm": ([C.POINTER(GemmArgs), vp], C.c_int),
+    "lp_qkv_post": ([vp, C.c_int, C.POINTER(QkvEpi), C.c_int, vp], C.c_int),
+    "lp_attention": ([C.POINTER(AttnArgs), vp], C.c_int),
+    "lp_attention_simt": ([C.POINTER(AttnArgs), vp], C.c_int),
+    "lp_cond_row": ([vp, C.c_int, vp, vp, C.c_int, vp, vp, C.c_int, vp, vp, C.c_int, vp], C.c_int),
+    "lp_add_row": ([vp, vp, vp, C.c_int, C.c_int, vp], C.c_int),
+    "lp_norm_mod": ([vp, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp, vp, C.c_int, vp], C.c_int),
+    "lp_sink_refresh": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_float, vp,
+                         C.POINTER(RopeGeom), vp, vp, C.c_int, C.c_int, i64, i64, vp], C.c_int),
+    "lp_silu": ([vp, vp, C.c_int, C.c_int, vp], C.c_int),
+    "lp_patchify": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
+    "lp_unpatchify_euler": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp],
+                            C.c_int),
+    "lp_history_noise": ([vp, C.c_int, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
+    "lp_randn": ([vp, i64, u64, u64, C.c_float, vp], C.c_int),
+    "lp_randn_bf16": ([vp, i64, u64, u64, C.c_float, vp], C.c_int),
+    "lp_link_send": ([vp, vp, i64, vp, vp, u32, C.c_int, vp, u64, vp], C.c_int),
+    "lp_link_recv": ([vp, vp, i64, vp, vp, u32, vp, u64, vp, vp], C.c_int),
+}
+
+
+class LivepipeError(RuntimeError):
+    """A liblivepipe_b200 entry point returned a non-zero status."""
+
+    def __init__(self, fn: str, code: int, msg: str):
+        super().__init__(f"{fn} failed (code {code}): {msg}")
+        self.code = code
+
+
+_lib = None
+_lock = threading.Lock()
+_inited_devices: set = set()
+
+
+def header_symbols() -> list:
+    """Entry points declared in include/livepipe_b200.h."""
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"LP_API\s+(?:int|const char\*)\s+(lp_\w+)\(", text)))
+
+
+def load() -> C.CDLL:
+    """Load the shared library (build it with `python -m paper_2512_04677_b200.build`)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is missing; build it with `python -m paper_2512_04677_b200.build` "
+                    "(there is no CPU fallback)")
+            lib = C.CDLL(LIB_PATH)
+            for name, (args, res) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = res
+            if lib.lp_abi_version() != 1:
+                raise ImportError("liblivepipe_b200 ABI version mismatch")
+            _lib = lib
+    return _lib
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != LP_OK:
+        msg = lib.lp_last_error().decode(errors="replace")
+        raise LivepipeError(name, rc, msg)
+
+
+def init_device(device: int) -> None:
+    if device in _inited_devices:
+        return
+    call("lp_init", device)
+    _inited_devices.add(device)

@@ -1,0 +1,363 @@
+// tcgen05 bf16 GEMM with fused epilogues (the projections of denoise_block:
+// QKV denoiser.py:240-242 + rotary :192-197, O :265, FFN :266, head :268).
+//
+//   C[M, N] = A[M, K] . W^T[N, K]^T     A, W^T bf16 K-major, fp32 accumulate
+//
+// Persistent, warp-specialised, one CTA per SM:
+//   warp 0      TMA producer (elected lane): A/B tiles -> 4-stage smem ring
+//   warp 1      TMEM allocator + MMA issuer (elected lane): tcgen05.mma
+//               128 x BN x 16 per instruction, accumulator in TMEM, double
+//               buffered (2 x BN columns) so the epilogue of tile t overlaps
+//               the main loop of tile t+1
+//   warps 2..5  epilogue: tcgen05.ld 32 rows x 32 columns per warp-load,
+//               fused STORE / RELU / GELU / gated RESIDUAL / QKV (per-head
+//               RMSNorm + rotary + scatter of k, v into the KV ring slot)
+#include "lp_common.cuh"
+#include "lp_sm100.cuh"
+#include "lp_tma.cuh"
+
+namespace lp {
+
+using namespace sm100;
+
+constexpr int GBM = 128, GBK = 64, GSTAGES = 4;
+constexpr int G_THREADS = 192;
+
+struct GemmParams {
+  int m, n, k;
+  int epilogue, out_dtype;
+  void* c;
+  int64_t ldc;
+  const float* bias;
+  const float* gate;
+  lp_qkv_epi qkv;
+};
+
+template <int BN>
+struct GemmSmem {
+  static constexpr int A_BYTES = GBM * GBK * 2;
+  static constexpr int B_BYTES = BN * GBK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = GSTAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + alignment slack
+};
+
+__device__ __forceinline__ void store_row32(void* out, int out_dtype, const float* v) {
+  if (out_dtype == LP_BF16) {
+    uint4* o = reinterpret_cast<uint4*>(out);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      o[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                        pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+  } else {
+    float4* o = reinterpret_cast<float4*>(out);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(G_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const GemmParams p) {
+  using SM = GemmSmem<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+  uint64_t* empty = full + GSTAGES;
+  uint64_t* tfull = empty + GSTAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tiles_m = (p.m + GBM - 1) / GBM, tiles_n = p.n / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = p.k / GBK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < GSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint64_t pol_a = l2_policy_evict_last();
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile % tiles_m) * GBM, n0 = (tile / tiles_m) * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * SM::STAGE_BYTES;
+          uint8_t* sb = sa + SM::A_BYTES;
+          mbar_arrive_expect_tx(&full[stage], SM::STAGE_BYTES);
+          tma_load_2d_hint(sa, &tmA, &full[stage], kb * GBK, m0, pol_a);
+          tma_load_2d(sb, &tmB, &full[stage], kb * GBK, n0);
+          if (++stage == GSTAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t IDESC = idesc_bf16_f32(GBM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t aphase = (local >> 1) & 1;
+      mbar_wait(&tempty[acc], aphase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_u32(smem + stage * SM::STAGE_BYTES);
+          const uint32_t sb = sa + SM::A_BYTES;
+          const uint64_t da = sdesc_kmajor_sw128(sa), db = sdesc_kmajor_sw128(sb);
+#pragma unroll
+          for (int k = 0; k < GBK / 16; ++k)
+            mma_bf16_ss(d_tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), IDESC, (kb | k) != 0);
+          mma_commit(&empty[stage]);
+          if (kb == num_kb - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == GSTAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5) ----------------
+    const int quarter = warp & 3;  // TMEM lanes [32*quarter, +32) are addressable by this warp
+    int local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t aphase = (local >> 1) & 1;
+      const int m0 = (tile % tiles_m) * GBM, n0 = (tile / tiles_m) * BN;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const int row = m0 + quarter * 32 + lane;
+      const bool valid = row < p.m;
+      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+
+      if (p.epilogue == LP_EPI_QKV) {
+        const lp_qkv_epi& e = p.qkv;
+        const int hd = e.head_dim;
+        const int section = n0 / e.d;  // 0 q, 1 k, 2 v
+        const int col0 = n0 - section * e.d;
+        int cur = e.desc->cur_row;
+        __nv_bfloat16* dst_base =
+            section == 0 ? reinterpret_cast<__nv_bfloat16*>(e.q_out) + (int64_t)row * e.d
+                         : reinterpret_cast<__nv_bfloat16*>(section == 1 ? e.k_arena : e.v_arena) +
+                               (int64_t)(cur + row) * e.d;
+        RopeTab rt{e.desc->rope_cos, e.desc->rope_sin, e.geom};
+        const float* g = section == 0 ? e.g_q : e.g_k;
+        for (int h0 = 0; h0 < BN; h0 += hd) {
+          float inv = 1.0f;
+          if (section < 2 && e.qk_norm) {
+            float ss = 0.0f;
+            for (int c0 = 0; c0 < hd; c0 += 32) {
+              uint32_t r[32];
+              tmem_ld32(tbase + h0 + c0, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                float v = __uint_as_float(r[j]);
+                ss += v * v;
+              }
+            }
+            inv = rsqrtf(ss / hd + e.eps);
+          }
+          for (int c0 = 0; c0 < hd; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tbase + h0 + c0, r);
+            tmem_ld_wait();
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            const int col = col0 + h0 + c0;  // column within the section
+            if (section < 2) {
+              if (e.qk_norm) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = v[j] * inv * (g ? g[col + j] : 1.0f);
+              }
+#pragma unroll
+              for (int j = 0; j < 32; j += 2) {
+                float cs, sn, xo, yo;
+                rt.get(row, (c0 + j) / 2, cs, sn);
+                rotate_pair(v[j], v[j + 1], cs, sn, xo, yo);
+                v[j] = xo;
+                v[j + 1] = yo;
+              }
+            }
+            if (valid) store_row32(dst_base + col, LP_BF16, v);
+          }
+        }
+      } else {
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c0, r);
+          tmem_ld_wait();
+          const int col = n0 + c0;
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          if (!valid) continue;
+          if (p.epilogue == LP_EPI_RESID) {
+            float* h = reinterpret_cast<float*>(p.c) + (int64_t)row * p.ldc + col;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 o = reinterpret_cast<float4*>(h)[q];
+              float g0 = 1.f, g1 = 1.f, g2 = 1.f, g3 = 1.f;
+              if (p.gate) {
+                float4 gg = reinterpret_cast<const float4*>(p.gate + col)[q];
+                g0 = gg.x; g1 = gg.y; g2 = gg.z; g3 = gg.w;
+              }
+              o.x += g0 * v[4 * q];
+              o.y += g1 * v[4 * q + 1];
+              o.z += g2 * v[4 * q + 2];
+              o.w += g3 * v[4 * q + 3];
+              reinterpret_cast<float4*>(h)[q] = o;
+            }
+          } else {
+            if (p.epilogue == LP_EPI_STORE && p.bias) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += p.bias[col + j];
+            } else if (p.epilogue == LP_EPI_RELU) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+            } else if (p.epilogue == LP_EPI_GELU) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = gelu_tanh_f(v[j]);
+            }
+            const int esz = p.out_dtype == LP_BF16 ? 2 : 4;
+            store_row32(reinterpret_cast<uint8_t*>(p.c) + ((int64_t)row * p.ldc + col) * esz, p.out_dtype, v);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+template <int BN>
+static int launch_gemm_tc(const lp_gemm_args* a, const GemmParams& p, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  int rc = make_tmap_bf16_2d(&ta, a->a, (uint64_t)a->m, (uint64_t)a->k, (uint64_t)a->lda, GBM, GBK);
+  if (rc) return rc;
+  rc = make_tmap_bf16_2d(&tb, a->w, (uint64_t)a->n, (uint64_t)a->k, (uint64_t)a->ldw, BN, GBK);
+  if (rc) return rc;
+  const int tiles = ((a->m + GBM - 1) / GBM) * (a->n / BN);
+  const int grid = std::min(tiles, std::max(1, num_sms()));
+  const int smem = GemmSmem<BN>::TOTAL;
+  auto kern = gemm_tc_kernel<BN>;
+  LP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<grid, G_THREADS, smem, st>>>(ta, tb, p);
+  return launch_status("gemm_tc");
+}
+
+int preload_gemm_tc() {
+  cudaFuncAttributes a;
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, gemm_tc_kernel<64>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, gemm_tc_kernel<128>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, gemm_tc_kernel<256>));
+  return LP_OK;
+}
+
+int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
+  LP_CHECK_ARG(num_sms() > 0, "lp_init() must be called before the tcgen05 GEMM");
+  LP_CHECK_ARG(a->k % GBK == 0, "gemm_tc: k must be a multiple of 64");
+  LP_CHECK_ARG(a->lda % 8 == 0 && a->ldw % 8 == 0, "gemm_tc: leading dims must be 16-byte aligned");
+  if (a->m == 0) return LP_OK;
+  GemmParams p;
+  p.m = a->m;
+  p.n = a->n;
+  p.k = a->k;
+  p.epilogue = a->epilogue;
+  p.out_dtype = a->out_dtype;
+  p.c = a->c;
+  p.ldc = a->ldc;
+  p.bias = a->bias;
+  p.gate = a->gate;
+  memset(&p.qkv, 0, sizeof(p.qkv));
+  if (a->epilogue == LP_EPI_QKV) {
+    LP_CHECK_ARG(a->qkv != nullptr, "gemm_tc: QKV epilogue needs qkv args");
+    p.qkv = *a->qkv;
+    LP_CHECK_ARG(a->n == 3 * p.qkv.d && p.qkv.head_dim % 32 == 0, "gemm_tc: QKV shape");
+    LP_CHECK_ARG(p.qkv.d % 256 == 0 || p.qkv.d % 128 == 0, "gemm_tc: QKV needs d % 128 == 0");
+    if (p.qkv.d % 256 == 0 && p.qkv.head_dim <= 256 && 256 % p.qkv.head_dim == 0)
+      return launch_gemm_tc<256>(a, p, st);
+    LP_CHECK_ARG(128 % p.qkv.head_dim == 0, "gemm_tc: head_dim must divide the tile");
+    return launch_gemm_tc<128>(a, p, st);
+  }
+  LP_CHECK_ARG(a->ldc % 4 == 0, "gemm_tc: ldc alignment");
+  if (a->n % 256 == 0) return launch_gemm_tc<256>(a, p, st);
+  if (a->n % 128 == 0) return launch_gemm_tc<128>(a, p, st);
+  if (a->n % 64 == 0) return launch_gemm_tc<64>(a, p, st);
+  return fail(LP_EUNSUPPORTED, "gemm_tc: n must be a multiple of 64");
+}
+
+// ------------------------------------------------------------------- TMA ---
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn g_encode = nullptr;
+
+int tma_init() {
+  if (g_encode) return LP_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  LP_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(LP_ECUDA, "cuTensorMapEncodeTiled not available");
+  g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+  return LP_OK;
+}
+
+int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                      uint32_t box_rows, uint32_t box_cols) {
+  if (!g_encode) return fail(LP_EINVAL, "TMA not initialised (call lp_init)");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapSwizzle sw = box_cols * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : box_cols * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                               : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LP_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return LP_OK;
+}
+
+}  // namespace lp

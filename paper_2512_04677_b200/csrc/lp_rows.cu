@@ -1,0 +1,386 @@
+// HBM-bound row kernels around the projections: conditioning row, norm +
+// AdaLN modulation, sink-frame refresh (RSFM), patch (un)embedding + Euler
+// step, history-noise injection and the device RNG.
+#include "lp_common.cuh"
+
+namespace lp {
+
+// ------------------------------------------------------------ cond row -----
+// c[col] = a.Wa[:,col] ; c += p.Wp[:,col] ; c += tau.Wt[:,col]
+// (denoiser.py:178-185: three pinned-order products summed in this order).
+__device__ __forceinline__ float dot_col(const float* x, int n, const float* w, int ldw, int col) {
+  float acc = 0.0f;
+  for (int k = 0; k < n; ++k) acc = __fadd_rn(acc, __fmul_rn(x[k], w[(int64_t)k * ldw + col]));
+  return acc;
+}
+
+__global__ void cond_row_kernel(const float* audio, int na, const float* wa, const float* prompt, int np,
+                                const float* wp, const float* tau, int nt, const float* wt, float* out,
+                                int d) {
+  int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= d) return;
+  float c = audio ? dot_col(audio, na, wa, d, col) : 0.0f;
+  c = __fadd_rn(c, dot_col(prompt, np, wp, d, col));
+  c = __fadd_rn(c, dot_col(tau, nt, wt, d, col));
+  out[col] = c;
+}
+
+// h[r,c] = x[r,c] + cond[c]   (denoiser.py:236)
+__global__ void add_row_kernel(const float* x, const float* c, float* h, int rows, int d) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)rows * d) return;
+  h[i] = __fadd_rn(x[i], c[i % d]);
+}
+
+// ------------------------------------------------------ norm + modulate ----
+template <int THREADS>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.0f;
+  if (threadIdx.x < THREADS / 32) t = red[threadIdx.x];
+  if (w == 0) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (l == 0) red[0] = t;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+// One CTA per row, float4 loads, two-pass mean/variance in fp32.
+template <typename OutT, int THREADS>
+__global__ void __launch_bounds__(THREADS) norm_mod_kernel(const float* __restrict__ h, int d, int mode,
+                                                           float eps, const float* __restrict__ shift,
+                                                           const float* __restrict__ scale,
+                                                           OutT* __restrict__ out) {
+  __shared__ float red[32];
+  const int64_t row = blockIdx.x;
+  const float* x = h + row * d;
+  OutT* o = out + row * d;
+  if (mode == 0) {
+    for (int c = threadIdx.x; c < d; c += THREADS) o[c] = from_f32<OutT>(x[c]);
+    return;
+  }
+  float s = 0.0f;
+  for (int c = threadIdx.x * 4; c < d; c += THREADS * 4) {
+    float4 v = *reinterpret_cast<const float4*>(x + c);
+    s += (v.x + v.y) + (v.z + v.w);
+  }
+  const float mu = block_sum<THREADS>(s, red) / d;
+  float q = 0.0f;
+  for (int c = threadIdx.x * 4; c < d; c += THREADS * 4) {
+    float4 v = *reinterpret_cast<const float4*>(x + c);
+    float a = v.x - mu, b = v.y - mu, e = v.z - mu, f = v.w - mu;
+    q += (a * a + b * b) + (e * e + f * f);
+  }
+  const float rstd = rsqrtf(block_sum<THREADS>(q, red) / d + eps);
+  for (int c = threadIdx.x * 4; c < d; c += THREADS * 4) {
+    float4 v = *reinterpret_cast<const float4*>(x + c);
+    float y[4] = {(v.x - mu) * rstd, (v.y - mu) * rstd, (v.z - mu) * rstd, (v.w - mu) * rstd};
+    if (mode == 2) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) y[j] = y[j] * (1.0f + scale[c + j]) + shift[c + j];
+    }
+    if constexpr (sizeof(OutT) == 2) {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(y[0], y[1]);
+      __nv_bfloat162 p1 = __floats2bfloat162_rn(y[2], y[3]);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&p0);
+      u.y = *reinterpret_cast<uint32_t*>(&p1);
+      *reinterpret_cast<uint2*>(o + c) = u;
+    } else {
+      *reinterpret_cast<float4*>(o + c) = make_float4(y[0], y[1], y[2], y[3]);
+    }
+  }
+}
+
+// ----------------------------------------------------------- sink refresh --
+// One warp per (sink token, head): optional RMSNorm(k) then rotation at the
+// sink position i + delta (kvcache.py:86-90, denoiser.py:249); v copied.
+template <typename T>
+__global__ void sink_refresh_kernel(const float* __restrict__ kraw, const float* __restrict__ vraw, int s_tok,
+                                    int d, int n_heads, int qk_norm, const float* __restrict__ g_k, float eps,
+                                    const lp_block_desc* __restrict__ desc, lp_rope_geom geom,
+                                    T* __restrict__ karena, T* __restrict__ varena, int64_t raw_stride,
+                                    int64_t arena_stride) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  const int tok = warp / n_heads, head = warp % n_heads;
+  if (tok >= s_tok) return;
+  const int layer = blockIdx.y;
+  kraw += layer * raw_stride;
+  vraw += layer * raw_stride;
+  karena += layer * arena_stride;
+  varena += layer * arena_stride;
+  if (g_k) g_k += (int64_t)layer * d;
+  const int hd = geom.head_dim;
+  const int row = desc->seg_row[0] + tok;
+  const float* k = kraw + (int64_t)tok * d + head * hd;
+  float inv = 1.0f;
+  if (qk_norm) {
+    float ss = 0.0f;
+    for (int c = lane; c < hd; c += 32) ss += k[c] * k[c];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    inv = rsqrtf(ss / hd + eps);
+  }
+  RopeTab rt{desc->sink_cos, desc->sink_sin, geom};
+  T* ko = karena + (int64_t)row * d + head * hd;
+  for (int p = lane; p < hd / 2; p += 32) {
+    float x = k[2 * p], y = k[2 * p + 1];
+    if (qk_norm) {
+      x = x * inv * (g_k ? g_k[head * hd + 2 * p] : 1.0f);
+      y = y * inv * (g_k ? g_k[head * hd + 2 * p + 1] : 1.0f);
+    }
+    float c, s, xo, yo;
+    rt.get(tok, p, c, s);
+    rotate_pair(x, y, c, s, xo, yo);
+    ko[2 * p] = from_f32<T>(xo);
+    ko[2 * p + 1] = from_f32<T>(yo);
+  }
+  const float* v = vraw + (int64_t)tok * d + head * hd;
+  T* vo = varena + (int64_t)row * d + head * hd;
+  for (int c = lane; c < hd; c += 32) vo[c] = from_f32<T>(v[c]);
+}
+
+// ------------------------------------------------------- patch embedding ---
+// x frames [F, C, H, W] -> tokens [(f, hp, wp), (c, py, px)]
+template <typename T>
+__global__ void patchify_kernel(const float* __restrict__ x, int frames, int C, int H, int W, int ph, int pw,
+                                T* __restrict__ tok) {
+  const int hp = H / ph, wp = W / pw, pd = C * ph * pw;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)frames * hp * wp * pd;
+  if (i >= total) return;
+  int e = (int)(i % pd);
+  int64_t t = i / pd;
+  int px = e % pw, py = (e / pw) % ph, c = e / (pw * ph);
+  int w = (int)(t % wp), hh = (int)((t / wp) % hp), f = (int)(t / ((int64_t)wp * hp));
+  tok[i] = from_f32<T>(x[(((int64_t)f * C + c) * H + hh * ph + py) * W + w * pw + px]);
+}
+
+// x_out = x + unpatchify(v) * dt   (latent.py:140-147: v*fp32(dt), then add)
+__global__ void unpatchify_euler_kernel(const float* __restrict__ x, const float* __restrict__ v, int frames,
+                                        int C, int H, int W, int ph, int pw,
+                                        const lp_block_desc* __restrict__ desc, float* __restrict__ xo) {
+  const int64_t total = (int64_t)frames * C * H * W;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const float dt = desc->dt;
+  float vv;
+  if (ph == 0) {
+    vv = v[i];
+  } else {
+    int xx = (int)(i % W), yy = (int)((i / W) % H), c = (int)((i / ((int64_t)W * H)) % C);
+    int f = (int)(i / ((int64_t)W * H * C));
+    const int hp = H / ph, wp = W / pw, pd = C * ph * pw;
+    int64_t t = ((int64_t)f * hp + yy / ph) * wp + xx / pw;
+    int e = (c * ph + yy % ph) * pw + xx % pw;
+    vv = v[t * pd + e];
+  }
+  xo[i] = __fadd_rn(x[i], __fmul_rn(vv, dt));
+}
+
+// ------------------------------------------------------------------- RNG ---
+// Philox4x32-10 (Salmon et al. 2011) + Box-Muller; counter = element / 4.
+struct Philox {
+  __device__ __forceinline__ static uint4 round(uint4 c, uint2 k) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+    uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+    return make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  __device__ __forceinline__ static uint4 gen(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      c = round(c, k);
+      k.x += 0x9E3779B9u;
+      k.y += 0xBB67AE85u;
+    }
+    return c;
+  }
+};
+
+__device__ __forceinline__ float4 normal4(uint64_t seed, uint64_t stream, uint64_t ctr) {
+  uint4 c = make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream, (uint32_t)(stream >> 32));
+  uint2 k = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  uint4 r = Philox::gen(c, k);
+  const float inv = 2.3283064365386963e-10f;  // 2^-32
+  float u0 = (r.x + 0.5f) * inv, u1 = (r.y + 0.5f) * inv, u2 = (r.z + 0.5f) * inv, u3 = (r.w + 0.5f) * inv;
+  float r0 = sqrtf(-2.0f * logf(u0)), r1 = sqrtf(-2.0f * logf(u2));
+  float s0, c0, s1, c1;
+  sincospif(2.0f * u1, &s0, &c0);
+  sincospif(2.0f * u3, &s1, &c1);
+  return make_float4(r0 * c0, r0 * s0, r1 * c1, r1 * s1);
+}
+
+template <typename T>
+__global__ void randn_kernel(T* out, int64_t n, uint64_t seed, uint64_t stream, float scale) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t i = q * 4;
+  if (i >= n) return;
+  float4 g = normal4(seed, stream, (uint64_t)q);
+  float v[4] = {g.x, g.y, g.z, g.w};
+  for (int j = 0; j < 4 && i + j < n; ++j) out[i + j] = from_f32<T>(v[j] * scale);
+}
+
+// History noise over the descriptor's history segments (kvcache.py:121-137):
+// dst rows = src rows + z * sigma (noise*sigma rounded, then the add).
+// Grid: x covers max history rows * d / 4 elements (packed over segments).
+template <typename T>
+__global__ void history_noise_kernel(T* __restrict__ arena, int d, const float* __restrict__ noise,
+                                     int n_layers, int layer, int kv, const lp_block_desc* __restrict__ desc) {
+  const float sigma = desc->sigma;
+  const int n_hist = desc->n_seg - 2;
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t i = q * 4;  // element index within the packed history
+  int64_t base = 0;
+  for (int e = 0; e < n_hist; ++e) {
+    const int s = e + 1;
+    const int64_t len = (int64_t)desc->seg_len[s] * d;
+    if (i < base + len) {
+      const int64_t off = i - base;
+      T* dst = arena + (int64_t)desc->seg_row[s] * d + off;
+      const T* src = arena + (int64_t)desc->src_row[s] * d + off;
+      float z[4];
+      if (noise) {
+        const float* zp = noise + ((((int64_t)e * 2 + kv) * n_layers + layer) * len) + off;
+        for (int j = 0; j < 4; ++j) z[j] = (off + j < len) ? zp[j] : 0.0f;
+      } else {
+        float4 g = normal4(desc->noise_key, ((uint64_t)(layer * 2 + kv) << 8) | (uint64_t)e, (uint64_t)(off >> 2));
+        z[0] = g.x; z[1] = g.y; z[2] = g.z; z[3] = g.w;
+      }
+      for (int j = 0; j < 4 && off + j < len; ++j)
+        dst[j] = from_f32<T>(__fadd_rn(to_f32(src[j]), __fmul_rn(z[j], sigma)));
+      return;
+    }
+    base += len;
+  }
+}
+
+// ---------------------------------------------------------------- launch ---
+static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+int preload_rows() {
+  cudaFuncAttributes a;
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, cond_row_kernel));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, add_row_kernel));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<float, 256>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<__nv_bfloat16, 256>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, sink_refresh_kernel<float>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, sink_refresh_kernel<__nv_bfloat16>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, patchify_kernel<float>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, patchify_kernel<__nv_bfloat16>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, unpatchify_euler_kernel));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_kernel<float>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_kernel<__nv_bfloat16>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, randn_kernel<float>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, randn_kernel<__nv_bfloat16>));
+  return LP_OK;
+}
+
+int cond_row(const float* audio, int na, const float* wa, const float* prompt, int np, const float* wp,
+             const float* tau, int nt, const float* wt, float* out, int d, cudaStream_t st) {
+  cond_row_kernel<<<nblk(d, 128), 128, 0, st>>>(audio, na, wa, prompt, np, wp, tau, nt, wt, out, d);
+  return launch_status("cond_row");
+}
+
+int add_row(const float* x, const float* c, float* h, int rows, int d, cudaStream_t st) {
+  int64_t n = (int64_t)rows * d;
+  if (n == 0) return LP_OK;
+  add_row_kernel<<<nblk(n, 256), 256, 0, st>>>(x, c, h, rows, d);
+  return launch_status("add_row");
+}
+
+int norm_mod(const float* h, int rows, int d, int mode, float eps, const float* shift, const float* scale,
+             void* out, int out_dtype, cudaStream_t st) {
+  LP_CHECK_ARG(mode == 0 || d % 4 == 0, "norm_mod: d must be a multiple of 4");
+  LP_CHECK_ARG(mode != 2 || (shift && scale), "norm_mod: modulation needs shift and scale");
+  if (rows == 0) return LP_OK;
+  if (out_dtype == LP_BF16)
+    norm_mod_kernel<__nv_bfloat16, 256><<<rows, 256, 0, st>>>(h, d, mode, eps, shift, scale,
+                                                               (__nv_bfloat16*)out);
+  else
+    norm_mod_kernel<float, 256><<<rows, 256, 0, st>>>(h, d, mode, eps, shift, scale, (float*)out);
+  return launch_status("norm_mod");
+}
+
+int sink_refresh(const float* kraw, const float* vraw, int s_tok, int d, int n_heads, int qk_norm,
+                 const float* g_k, float eps, const lp_block_desc* desc, const lp_rope_geom& geom, void* karena,
+                 void* varena, int dtype, int n_layers, int64_t raw_stride, int64_t arena_stride,
+                 cudaStream_t st) {
+  const int warps = s_tok * n_heads;
+  if (warps == 0 || n_layers == 0) return LP_OK;
+  dim3 grid(nblk((int64_t)warps * 32, 128), n_layers);
+  if (dtype == LP_BF16)
+    sink_refresh_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(kraw, vraw, s_tok, d, n_heads, qk_norm, g_k, eps,
+                                                             desc, geom, (__nv_bfloat16*)karena,
+                                                             (__nv_bfloat16*)varena, raw_stride, arena_stride);
+  else
+    sink_refresh_kernel<float><<<grid, 128, 0, st>>>(kraw, vraw, s_tok, d, n_heads, qk_norm, g_k, eps, desc, geom,
+                                                     (float*)karena, (float*)varena, raw_stride, arena_stride);
+  return launch_status("sink_refresh");
+}
+
+template <typename T>
+__global__ void silu_kernel(const float* x, T* out, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = from_f32<T>(x[i] / (1.0f + expf(-x[i])));
+}
+
+int silu(const float* x, void* out, int n, int dtype, cudaStream_t st) {
+  if (n == 0) return LP_OK;
+  if (dtype == LP_BF16)
+    silu_kernel<__nv_bfloat16><<<nblk(n, 256), 256, 0, st>>>(x, (__nv_bfloat16*)out, n);
+  else
+    silu_kernel<float><<<nblk(n, 256), 256, 0, st>>>(x, (float*)out, n);
+  return launch_status("silu");
+}
+
+int patchify(const float* x, int frames, int C, int H, int W, int ph, int pw, void* tok, int dtype,
+             cudaStream_t st) {
+  LP_CHECK_ARG(ph > 0 && pw > 0 && H % ph == 0 && W % pw == 0, "patchify: bad patch");
+  int64_t n = (int64_t)frames * C * H * W;
+  if (dtype == LP_BF16)
+    patchify_kernel<__nv_bfloat16><<<nblk(n, 256), 256, 0, st>>>(x, frames, C, H, W, ph, pw, (__nv_bfloat16*)tok);
+  else
+    patchify_kernel<float><<<nblk(n, 256), 256, 0, st>>>(x, frames, C, H, W, ph, pw, (float*)tok);
+  return launch_status("patchify");
+}
+
+int unpatchify_euler(const float* x, const float* v, int frames, int C, int H, int W, int ph, int pw,
+                     const lp_block_desc* desc, float* xo, cudaStream_t st) {
+  int64_t n = (int64_t)frames * C * H * W;
+  unpatchify_euler_kernel<<<nblk(n, 256), 256, 0, st>>>(x, v, frames, C, H, W, ph, pw, desc, xo);
+  return launch_status("unpatchify_euler");
+}
+
+int history_noise(void* arena, int dtype, int d, const float* noise, int n_layers, int layer, int kv,
+                  const lp_block_desc* desc, int max_rows, cudaStream_t st) {
+  LP_CHECK_ARG(d % 4 == 0, "history_noise: d must be a multiple of 4");
+  int64_t n = (int64_t)max_rows * d;
+  if (n == 0) return LP_OK;
+  int blocks = nblk((n + 3) / 4, 256);
+  if (dtype == LP_BF16)
+    history_noise_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((__nv_bfloat16*)arena, d, noise, n_layers, layer,
+                                                                kv, desc);
+  else
+    history_noise_kernel<float><<<blocks, 256, 0, st>>>((float*)arena, d, noise, n_layers, layer, kv, desc);
+  return launch_status("history_noise");
+}
+
+int randn(void* out, int64_t n, uint64_t seed, uint64_t stream, float scale, int dtype, cudaStream_t st) {
+  if (n == 0) return LP_OK;
+  int blocks = nblk((n + 3) / 4, 256);
+  if (dtype == LP_BF16)
+    randn_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((__nv_bfloat16*)out, n, seed, stream, scale);
+  else
+    randn_kernel<float><<<blocks, 256, 0, st>>>((float*)out, n, seed, stream, scale);
+  return launch_status("randn");
+}
+
+}  // namespace lp

@@ -1,0 +1,143 @@
+"""tcgen05 GEMM (lp_gemm, LP_BF16) against a torch fp32 reference on the
+same bf16 operands, for every epilogue; plus the fp32 pinned GEMM against
+the reference's ascending-k order (bitwise)."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2512_04677_b200 import _lib as L
+from paper_2512_04677_b200.numerics import spatial_tables
+
+from gpu_helpers import make_desc, rel_l2, rope_ref, upload_desc
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _init():
+    L.init_device(0)
+
+
+def _gemm(a, w_t, c, epi, out_dtype, bias=None, gate=None, qkv=None, in_dtype=L.LP_BF16):
+    args = L.GemmArgs()
+    args.in_dtype, args.out_dtype, args.epilogue = in_dtype, out_dtype, epi
+    args.m, args.k = a.shape
+    args.n = w_t.shape[0] if in_dtype == L.LP_BF16 else w_t.shape[1]
+    args.lda, args.ldw = a.shape[1], w_t.shape[1]
+    args.ldc = c.shape[1] if c is not None else 0
+    args.a, args.w = a.data_ptr(), w_t.data_ptr()
+    args.c = c.data_ptr() if c is not None else None
+    args.bias = bias.data_ptr() if bias is not None else None
+    args.gate = gate.data_ptr() if gate is not None else None
+    args.qkv = C.pointer(qkv) if qkv is not None else None
+    L.call("lp_gemm", C.byref(args), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+
+
+def _ab(m, k, n, seed=0):
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    a = torch.randn((m, k), generator=g, device=DEV).to(torch.bfloat16)
+    w = (torch.randn((n, k), generator=g, device=DEV) / k ** 0.5).to(torch.bfloat16)
+    return a, w
+
+
+@pytest.mark.parametrize("m,k,n", [(128, 64, 256), (300, 256, 512), (4680 // 4, 512, 384), (77, 1024, 64),
+                                   (1, 512, 768), (1000, 128, 128)])
+def test_store_bf16_and_f32(m, k, n):
+    a, w = _ab(m, k, n)
+    ref = a.float() @ w.float().T
+    c32 = torch.zeros((m, n), device=DEV)
+    _gemm(a, w, c32, L.EPI_STORE, L.LP_F32)
+    assert rel_l2(c32.cpu(), ref.cpu()) < 1e-5
+    c16 = torch.zeros((m, n), device=DEV, dtype=torch.bfloat16)
+    bias = torch.randn(n, device=DEV)
+    _gemm(a, w, c16, L.EPI_STORE, L.LP_BF16, bias=bias)
+    assert rel_l2(c16.float().cpu(), (ref + bias).cpu()) < 5e-3
+
+
+@pytest.mark.parametrize("epi", [L.EPI_RELU, L.EPI_GELU])
+def test_activation_epilogues(epi):
+    m, k, n = 333, 320, 768
+    a, w = _ab(m, k, n, 1)
+    ref = a.float() @ w.float().T
+    ref = torch.relu(ref) if epi == L.EPI_RELU else torch.nn.functional.gelu(ref, approximate="tanh")
+    c = torch.zeros((m, n), device=DEV, dtype=torch.bfloat16)
+    _gemm(a, w, c, epi, L.LP_BF16)
+    assert rel_l2(c.float().cpu(), ref.cpu()) < 5e-3
+
+
+def test_gated_residual_epilogue():
+    m, k, n = 250, 448, 256
+    a, w = _ab(m, k, n, 2)
+    h = torch.randn((m, n), device=DEV)
+    gate = torch.randn(n, device=DEV)
+    ref = h + gate * (a.float() @ w.float().T)
+    _gemm(a, w, h, L.EPI_RESID, L.LP_F32, gate=gate)
+    assert rel_l2(h.cpu(), ref.cpu()) < 1e-5
+
+
+@pytest.mark.parametrize("qk_norm,spatial", [(False, False), (True, True)])
+def test_qkv_epilogue(qk_norm, spatial):
+    n_heads, hd = 4, 128
+    d = n_heads * hd
+    n_tok = 390 if spatial else 200
+    a, w = _ab(n_tok, d, 3 * d, 3)
+    if spatial:
+        third = hd // 6
+        t_dim, dh, dw = hd - 4 * third, 2 * third, 2 * third
+        gh, gw = 5, 26  # 130 tokens per frame, 3 frames
+        sc, ss = spatial_tables(gh, gw, dh, dw, 10000.0)
+    else:
+        t_dim, dh, dw, gh, gw = hd, 0, 0, 1, 1
+        sc = ss = np.zeros((1, 0), np.float32)
+    spc, sps = torch.from_numpy(sc).to(DEV), torch.from_numpy(ss).to(DEV)
+    rows = 1000
+    karena = torch.zeros((rows, d), device=DEV, dtype=torch.bfloat16)
+    varena = torch.zeros_like(karena)
+    q = torch.zeros((n_tok, d), device=DEV, dtype=torch.bfloat16)
+    cur = 300
+    desc = make_desc(7, [(0, 10), (cur, n_tok)], cur, n_tok, t_dim)
+    ddev = upload_desc(desc)
+    g_q = (1 + 0.1 * torch.randn(d, device=DEV)) if qk_norm else None
+    g_k = (1 + 0.1 * torch.randn(d, device=DEV)) if qk_norm else None
+    geom = L.RopeGeom(hd, t_dim // 2, gh * gw, (dh + dw) // 2, spc.data_ptr(), sps.data_ptr())
+    epi = L.QkvEpi(d, n_heads, hd, int(qk_norm), 1e-6, g_q.data_ptr() if qk_norm else 0,
+                   g_k.data_ptr() if qk_norm else 0, q.data_ptr(), karena.data_ptr(), varena.data_ptr(),
+                   ddev.data_ptr(), geom)
+    _gemm(a, w, None, L.EPI_QKV, L.LP_BF16, qkv=epi)
+    y = a.float() @ w.float().T
+    qr, kr, vr = y[:, :d], y[:, d:2 * d], y[:, 2 * d:]
+
+    def norm(x, g):
+        if not qk_norm:
+            return x
+        xh = x.reshape(n_tok, n_heads, hd)
+        xh = xh * torch.rsqrt((xh * xh).mean(-1, keepdim=True) + 1e-6)
+        return xh.reshape(n_tok, d) * g
+
+    tc = np.array(desc.rope_cos[: t_dim // 2], np.float32)
+    ts = np.array(desc.rope_sin[: t_dim // 2], np.float32)
+    qref = rope_ref(norm(qr, g_q), n_heads, hd, tc, ts, spc, sps, gh * gw)
+    kref = rope_ref(norm(kr, g_k), n_heads, hd, tc, ts, spc, sps, gh * gw)
+    assert rel_l2(q.float().cpu(), qref.cpu()) < 5e-3
+    assert rel_l2(karena[cur:cur + n_tok].float().cpu(), kref.cpu()) < 5e-3
+    assert rel_l2(varena[cur:cur + n_tok].float().cpu(), vr.cpu()) < 5e-3
+    assert karena[:cur].abs().sum().item() == 0 and karena[cur + n_tok:].abs().sum().item() == 0
+
+
+def test_f32_pinned_gemm_is_bitwise_reference_order():
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((37, 70)).astype(np.float32)
+    b = rng.standard_normal((70, 45)).astype(np.float32)
+    ref = np.zeros((37, 45), np.float32)
+    for kk in range(70):
+        ref += np.multiply.outer(a[:, kk], b[kk])
+    ta, tb = torch.from_numpy(a).to(DEV), torch.from_numpy(b).to(DEV)
+    c = torch.zeros((37, 45), device=DEV)
+    _gemm(ta, tb, c, L.EPI_STORE, L.LP_F32, in_dtype=L.LP_F32)
+    assert c.cpu().numpy().tobytes() == ref.tobytes()
