@@ -1,23 +1,29 @@
 // tcgen05 flash attention over the RSFM key set [sink | history ring | current]
 // (denoiser.py:246-264, _attend_head :152-158, softmax numerics.py:67-78).
 //
-// One CTA per (128-query tile, head).  Head dim 128, bf16 Q/K/V, fp32 S/O in
-// TMEM, online softmax in fp32.  KV tiles of 128 keys walk the descriptor's
-// segments in reference order (sink, oldest -> newest history, current); the
-// ragged tail of each segment is masked to -inf, so segments need no padding
-// and no K/V is gathered or copied.
+// One CTA per (256 queries, head): two 128-row Q tiles (A, B) share every
+// K/V tile.  Head dim 128, bf16 Q/K/V, fp32 S/O in TMEM, online softmax in
+// fp32.  KV tiles of 128 keys walk the descriptor's segments in reference
+// order (sink, oldest -> newest history, current); the ragged tail of a
+// segment is masked to -inf, so segments need no padding and nothing is
+// gathered or copied.
 //
-//   warp 0      TMA producer: Q once, then K_j (2-stage ring) and V_{j-1}
-//               (2-stage ring; V lags K by one tile so K never waits on V)
-//   warp 1      TMEM allocator + MMA issuer: S_{j+1} = Q K_{j+1}^T is issued
-//               before P_j V_j so the tensor core works on the next tile while
-//               the softmax warps process this one (S double-buffered in TMEM)
-//   warps 2..5  softmax / correction / epilogue: thread = query row; S row
-//               from TMEM (two passes: max, then exp2), P (bf16) -> smem in
-//               the UMMA K-major SW128 layout, O rescaled in TMEM when the
-//               running max grows, O / l -> bf16 output at the end
+//   warp 0      TMA producer: Q_A, Q_B once, then K_j (2-stage ring) and
+//               V_{j-1} (2-stage ring, lagging K by one tile)
+//   warp 1      TMEM allocator + MMA issuer (one elected lane):
+//                 S_A(j+1) and S_B(j+1) = Q K^T are issued right after
+//                 P_A(j) V_j / P_B(j) V_j, so the tensor core always has the
+//                 other tile's work while a softmax warpgroup runs
+//   warps 2-5   softmax warpgroup A, warps 6-9 softmax warpgroup B: thread =
+//               query row; S row from TMEM in one pass, exp2 with a lazily
+//               updated running max (O is rescaled in TMEM only when the max
+//               grows by more than 2^8), P written back to TMEM as bf16 over
+//               its own S columns and consumed from TMEM by the P.V MMA
+//               (A-operand-in-TMEM form), O / l -> bf16 at the end
 //
-// TMEM columns: S0 [0,128) S1 [128,256) O [256,384).
+// TMEM columns: S_A|P_A [0,128)  S_B|P_B [128,256)  O_A [256,384)  O_B [384,512).
+// In-order completion of one thread's tcgen05.mma stream makes the S(j+1)
+// write after P(j).V safe, and s_full(j) imply P(j-1).V done.
 #include "lp_common.cuh"
 #include "lp_sm100.cuh"
 #include "lp_tma.cuh"
@@ -26,19 +32,19 @@ namespace lp {
 
 using namespace sm100;
 
-constexpr int AT_M = 128;      // query rows per CTA
+constexpr int AT_M = 128;      // query rows per softmax warpgroup
 constexpr int AT_N = 128;      // keys per tile
 constexpr int AT_D = 128;      // head dim
-constexpr int AT_THREADS = 192;
-constexpr int AT_TILE_BYTES = AT_N * AT_D * 2;  // 32 KB: K tile, V tile, Q tile, P tile
+constexpr int AT_THREADS = 320;
+constexpr int AT_TILE_BYTES = AT_N * AT_D * 2;  // 32 KB
 constexpr int AT_HALF = AT_TILE_BYTES / 2;      // one 64-column SW128 block
+constexpr float AT_RESCALE_THRESH = 8.0f;       // log2 units: rescale O when the max grows > 2^8
 
 struct AttnSmem {
-  static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = Q_OFF + AT_TILE_BYTES;
-  static constexpr int V_OFF = K_OFF + 2 * AT_TILE_BYTES;
-  static constexpr int P_OFF = V_OFF + 2 * AT_TILE_BYTES;
-  static constexpr int BAR_OFF = P_OFF + AT_TILE_BYTES;
+  static constexpr int Q_OFF = 0;                           // Q_A, Q_B
+  static constexpr int K_OFF = Q_OFF + 2 * AT_TILE_BYTES;   // 2 stages
+  static constexpr int V_OFF = K_OFF + 2 * AT_TILE_BYTES;   // 2 stages
+  static constexpr int BAR_OFF = V_OFF + 2 * AT_TILE_BYTES;
   static constexpr int SEG_OFF = BAR_OFF + 256;
   static constexpr int TOTAL = SEG_OFF + 2 * LP_MAX_SEG * 4 + 16 + 1024;
 };
@@ -60,7 +66,6 @@ struct TileCursor {
     row = r; len = l; n_seg = n; seg = 0; off = 0;
     while (seg < n_seg && len[seg] == 0) ++seg;
   }
-  __device__ bool valid() const { return seg < n_seg; }
   __device__ int cur_row() const { return row[seg] + off; }
   __device__ int cur_valid() const { return min(AT_N, len[seg] - off); }
   __device__ void next() {
@@ -73,8 +78,20 @@ struct TileCursor {
   }
 };
 
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void tmem_st32_x(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
 }
 
 __global__ void __launch_bounds__(AT_THREADS, 1)
@@ -88,10 +105,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint64_t* k_empty = bars + 3;  // [2]
   uint64_t* v_full = bars + 5;   // [2]
   uint64_t* v_empty = bars + 7;  // [2]
-  uint64_t* s_full = bars + 9;   // [2]
-  uint64_t* s_free = bars + 11;  // [2]
-  uint64_t* p_full = bars + 13;
-  uint64_t* o_done = bars + 14;  // [2]
+  uint64_t* s_full = bars + 9;   // [2] per Q tile
+  uint64_t* p_full = bars + 11;  // [2] per Q tile
+  uint64_t* o_done = bars + 13;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
   int* seg_row = reinterpret_cast<int*>(smem + AttnSmem::SEG_OFF);
   int* seg_len = seg_row + LP_MAX_SEG;
@@ -99,7 +115,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int head = blockIdx.y;
-  const int q0 = blockIdx.x * AT_M;
+  const int q0 = blockIdx.x * (2 * AT_M);
 
   const int nseg = min(p.desc->n_seg, LP_MAX_SEG);
   for (int s = threadIdx.x; s < nseg; s += blockDim.x) {
@@ -123,10 +139,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
-      mbar_init(&o_done[i], 1);
+      mbar_init(&p_full[i], 4);
     }
-    mbar_init(p_full, 4);
+    mbar_init(o_done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -141,9 +156,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     // ------------------------------------------------ TMA producer
     if (elect_one()) {
       uint8_t* sq = smem + AttnSmem::Q_OFF;
-      mbar_arrive_expect_tx(q_full, AT_TILE_BYTES);
-      tma_load_2d(sq, &tmQ, q_full, col0, q0);
-      tma_load_2d(sq + AT_HALF, &tmQ, q_full, col0 + 64, q0);
+      mbar_arrive_expect_tx(q_full, 2 * AT_TILE_BYTES);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        tma_load_2d(sq + t * AT_TILE_BYTES, &tmQ, q_full, col0, q0 + t * AT_M);
+        tma_load_2d(sq + t * AT_TILE_BYTES + AT_HALF, &tmQ, q_full, col0 + 64, q0 + t * AT_M);
+      }
       TileCursor ck, cv;
       ck.init(seg_row, seg_len, n_seg_s[0]);
       cv.init(seg_row, seg_len, n_seg_s[0]);
@@ -171,144 +189,150 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    constexpr uint32_t IDESC_S = idesc_bf16_f32(AT_M, AT_N);                 // Q K^T: both K-major
-    constexpr uint32_t IDESC_O = idesc_bf16_f32(AT_M, AT_D, false, true);    // P V: V is MN-major
+    constexpr uint32_t IDESC_S = idesc_bf16_f32(AT_M, AT_N);               // Q K^T: both K-major
+    constexpr uint32_t IDESC_O = idesc_bf16_f32(AT_M, AT_D, false, true);  // P V: P in TMEM, V MN-major
     const uint32_t sq = smem_u32(smem + AttnSmem::Q_OFF);
-    const uint32_t sp = smem_u32(smem + AttnSmem::P_OFF);
-    const uint32_t t_o = tmem_base + 256;
-    auto issue_s = [&](int t) {
-      const int b = t & 1;
-      mbar_wait(&k_full[b], (t >> 1) & 1);
-      if (t >= 2) mbar_wait(&s_free[b], ((t >> 1) - 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sk = smem_u32(smem + AttnSmem::K_OFF + b * AT_TILE_BYTES);
+    auto issue_s = [&](int t, int x) {  // S_x(t) = Q_x K_t^T
+      const uint32_t sk = smem_u32(smem + AttnSmem::K_OFF + (t & 1) * AT_TILE_BYTES);
+      const uint32_t sqx = sq + x * AT_TILE_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < AT_D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * AT_HALF + (kk & 3) * 32;
-          mma_bf16_ss(tmem_base + b * AT_N, sdesc_kmajor_sw128(sq + off), sdesc_kmajor_sw128(sk + off), IDESC_S,
-                      kk != 0);
-        }
-        mma_commit(&k_empty[b]);
-        mma_commit(&s_full[b]);
+      for (int kk = 0; kk < AT_D / 16; ++kk) {
+        const uint32_t off = (kk >> 2) * AT_HALF + (kk & 3) * 32;
+        mma_bf16_ss(tmem_base + x * AT_N, sdesc_kmajor_sw128(sqx + off), sdesc_kmajor_sw128(sk + off), IDESC_S,
+                    kk != 0);
       }
-      __syncwarp();
+    };
+    auto issue_pv = [&](int t, int x) {  // O_x += P_x(t) V_t
+      const uint32_t sv = smem_u32(smem + AttnSmem::V_OFF + (t & 1) * AT_TILE_BYTES);
+      const uint32_t tp = tmem_base + x * AT_N;        // P_x: 64 columns of packed bf16 pairs
+      const uint32_t to = tmem_base + 256 + x * AT_D;  // O_x
+#pragma unroll
+      for (int kk = 0; kk < AT_N / 16; ++kk)
+        mma_bf16_ts(to, tp + kk * 8, sdesc_mnmajor_sw128(sv + kk * 16 * 128, AT_HALF), IDESC_O, (t | kk) != 0);
     };
     mbar_wait(q_full, 0);
-    if (n_tiles > 0) issue_s(0);
-    for (int j = 0; j < n_tiles; ++j) {
-      if (j + 1 < n_tiles) issue_s(j + 1);
-      const int b = j & 1;
-      mbar_wait(p_full, j & 1);
-      mbar_wait(&v_full[b], (j >> 1) & 1);
+    if (n_tiles > 0) {
+      mbar_wait(&k_full[0], 0);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t sv = smem_u32(smem + AttnSmem::V_OFF + b * AT_TILE_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < AT_N / 16; ++kk) {
-          const uint32_t aoff = (kk >> 2) * AT_HALF + (kk & 3) * 32;  // P: K-major over keys
-          const uint32_t boff = kk * 16 * 128;                         // V: 16 key rows of 128 B
-          mma_bf16_ss(t_o, sdesc_kmajor_sw128(sp + aoff), sdesc_mnmajor_sw128(sv + boff, AT_HALF), IDESC_O,
-                      (j | kk) != 0);
-        }
-        mma_commit(&v_empty[b]);
-        mma_commit(&o_done[b]);
+        issue_s(0, 0);
+        mma_commit(&s_full[0]);
+        issue_s(0, 1);
+        mma_commit(&s_full[1]);
+        mma_commit(&k_empty[0]);
       }
       __syncwarp();
     }
+    for (int j = 0; j < n_tiles; ++j) {
+      const bool more = j + 1 < n_tiles;
+      // tile A: P_A(j) V_j, then S_A(j+1)
+      mbar_wait(&p_full[0], j & 1);
+      mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+      if (more) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        issue_pv(j, 0);
+        if (more) {
+          issue_s(j + 1, 0);
+          mma_commit(&s_full[0]);
+        }
+      }
+      __syncwarp();
+      // tile B: P_B(j) V_j, then S_B(j+1)
+      mbar_wait(&p_full[1], j & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        issue_pv(j, 1);
+        mma_commit(&v_empty[j & 1]);
+        if (more) {
+          issue_s(j + 1, 1);
+          mma_commit(&s_full[1]);
+          mma_commit(&k_empty[(j + 1) & 1]);
+        }
+      }
+      __syncwarp();
+    }
+    if (elect_one()) mma_commit(o_done);
+    __syncwarp();
   } else {
-    // ------------------------------------------------ softmax warps
-    const int quarter = warp & 3;
-    const int r = quarter * 32 + lane;  // row within the tile == TMEM lane
+    // ------------------------------------------------ softmax warpgroups
+    const int x = (warp - 2) / 4;        // Q tile: 0 = A (warps 2-5), 1 = B (warps 6-9)
+    const int quarter = warp & 3;        // TMEM lane quarter accessible to this warp
+    const int r = quarter * 32 + lane;   // row within the Q tile == TMEM lane
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const uint32_t t_o = tmem_base + lane_base + 256;
-    uint8_t* sp = smem + AttnSmem::P_OFF;
+    const uint32_t t_s = tmem_base + lane_base + x * AT_N;
+    const uint32_t t_o = tmem_base + lane_base + 256 + x * AT_D;
+    const float sc = p.scale_log2;
     float m_run = -INFINITY, l_run = 0.0f;
     TileCursor cs;
     cs.init(seg_row, seg_len, n_seg_s[0]);
     for (int j = 0; j < n_tiles; ++j, cs.next()) {
-      const int b = j & 1;
       const int nvalid = cs.cur_valid();
-      const uint32_t t_s = tmem_base + lane_base + b * AT_N;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
+      mbar_wait(&s_full[x], j & 1);
       tc_fence_after();
-      // pass 1: row max of the valid columns
-      float mx = -INFINITY;
-#pragma unroll 1
-      for (int c0 = 0; c0 < AT_N; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(t_s + c0, v);
-        tmem_ld_wait();
+      uint32_t s[128];
+      tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+      tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+      tmem_ld32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
+      tmem_ld32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
+      tmem_ld_wait();
+      if (nvalid < AT_N) {  // ragged segment tail (warp-uniform)
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c0 + i < nvalid) mx = fmaxf(mx, __uint_as_float(v[i]));
+        for (int i = 0; i < 128; ++i)
+          if (i >= nvalid) s[i] = __float_as_uint(-INFINITY);
       }
-      const float m_new = fmaxf(m_run, mx * p.scale_log2);
-      const float alpha = exp2f(m_run - m_new);  // 0 on the first tile (m_run = -inf)
-      // pass 2: p = exp2(s*scale*log2e - m_new), packed bf16
+      float mx = __uint_as_float(s[0]);
+#pragma unroll
+      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, __uint_as_float(s[i]));
+      const float m_tile = mx * sc;
+      float alpha = 1.0f;
+      bool rescale = false;
+      if (j == 0) {
+        m_run = m_tile;
+      } else {
+        const bool need = m_tile > m_run + AT_RESCALE_THRESH;
+        rescale = __any_sync(0xffffffffu, need);
+        if (need) {
+          alpha = ex2(m_run - m_tile);
+          m_run = m_tile;
+        }
+      }
+      // p = 2^(s*scale*log2e - m), packed to bf16 pairs in key order
+      float rs0 = 0.f, rs1 = 0.f;
       uint32_t pk[64];
-      float rs = 0.0f;
 #pragma unroll
-      for (int c0 = 0; c0 < AT_N; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(t_s + c0, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          float e0 = (c0 + i < nvalid) ? exp2f(__uint_as_float(v[i]) * p.scale_log2 - m_new) : 0.0f;
-          float e1 = (c0 + i + 1 < nvalid) ? exp2f(__uint_as_float(v[i + 1]) * p.scale_log2 - m_new) : 0.0f;
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
-          rs += __low2float(h2) + __high2float(h2);
-          pk[(c0 + i) / 2] = *reinterpret_cast<uint32_t*>(&h2);
-        }
+      for (int i = 0; i < 128; i += 2) {
+        const float e0 = ex2(fmaf(__uint_as_float(s[i]), sc, -m_run));
+        const float e1 = ex2(fmaf(__uint_as_float(s[i + 1]), sc, -m_run));
+        rs0 += e0;
+        rs1 += e1;
+        pk[i / 2] = pack_bf16(e0, e1);
       }
-      // S buffer b may now be overwritten by S_{j+2}
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[b]);
-      l_run = l_run * alpha + rs;
-      m_run = m_new;
-      // PV_{j-1} must be complete before O is rescaled and P is overwritten
-      if (j >= 1) {
-        mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.0f)) {
+      l_run = l_run * alpha + (rs0 + rs1);
+      tmem_st32_x(t_s + 0, &pk[0]);
+      tmem_st32_x(t_s + 32, &pk[32]);
+      if (rescale) {
+        // P(j-1).V is complete (implied by s_full(j)); O_x is idle until p_full(j)
 #pragma unroll 1
-          for (int c0 = 0; c0 < AT_D; c0 += 32) {
-            uint32_t v[32];
-            tmem_ld32(t_o + c0, v);
-            tmem_ld_wait();
+        for (int c0 = 0; c0 < AT_D; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(t_o + c0, v);
+          tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-            tmem_st32(t_o + c0, v);
-          }
-          tmem_st_wait();
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+          tmem_st32(t_o + c0, v);
         }
       }
-      // P row r -> smem, UMMA K-major SW128: block kb = keys [64kb, 64kb+64),
-      // row r at 128 B, 16-byte chunk c stored at chunk c ^ (r % 8)
-#pragma unroll
-      for (int kb = 0; kb < 2; ++kb) {
-        uint8_t* rowp = sp + kb * AT_HALF + r * 128;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int src = kb * 32 + c * 4;
-          *reinterpret_cast<uint4*>(rowp + ((c ^ (r & 7)) * 16)) =
-              make_uint4(pk[src], pk[src + 1], pk[src + 2], pk[src + 3]);
-        }
-      }
-      fence_proxy_async_smem();
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[x]);
     }
     // epilogue: O / l -> bf16
-    if (n_tiles > 0) {
-      mbar_wait(&o_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
-      tc_fence_after();
-    }
+    mbar_wait(o_done, 0);
+    tc_fence_after();
     const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
-    const int row = q0 + r;
+    const int row = q0 + x * AT_M + r;
 #pragma unroll 1
     for (int c0 = 0; c0 < AT_D; c0 += 32) {
       uint32_t v[32];
@@ -359,7 +383,7 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
   p.out = static_cast<__nv_bfloat16*>(a->out);
   p.ldo = d;
   p.desc = a->desc;
-  dim3 grid((a->n_q + AT_M - 1) / AT_M, a->n_heads);
+  dim3 grid((a->n_q + 2 * AT_M - 1) / (2 * AT_M), a->n_heads);
   const int smem = AttnSmem::TOTAL;
   LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   attn_tc_kernel<<<grid, AT_THREADS, smem, st>>>(tq, tk, tv, p);
