@@ -198,15 +198,19 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
             const int col = col0 + h0 + c0;  // column within the section
             if (section < 2) {
+              float cs[16], sn[16], gg[32];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) rt.get(row, c0 / 2 + j, cs[j], sn[j]);
               if (e.qk_norm) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = v[j] * inv * (g ? g[col + j] : 1.0f);
+                for (int j = 0; j < 32; ++j) gg[j] = g ? __ldg(g + col + j) * inv : inv;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] *= gg[j];
               }
 #pragma unroll
               for (int j = 0; j < 32; j += 2) {
-                float cs, sn, xo, yo;
-                rt.get(row, (c0 + j) / 2, cs, sn);
-                rotate_pair(v[j], v[j + 1], cs, sn, xo, yo);
+                float xo, yo;
+                rotate_pair(v[j], v[j + 1], cs[j / 2], sn[j / 2], xo, yo);
                 v[j] = xo;
                 v[j + 1] = yo;
               }
@@ -225,21 +229,28 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
           if (!valid) continue;
           if (p.epilogue == LP_EPI_RESID) {
-            float* h = reinterpret_cast<float*>(p.c) + (int64_t)row * p.ldc + col;
+            // all loads first (h and gate may alias as far as the compiler
+            // knows; interleaving loads with stores serialises DRAM round trips)
+            float4* h = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.c) + (int64_t)row * p.ldc + col);
+            float4 o[8], g[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] = __ldcs(h + q);
+            if (p.gate) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) g[q] = __ldg(reinterpret_cast<const float4*>(p.gate + col) + q);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) g[q] = make_float4(1.f, 1.f, 1.f, 1.f);
+            }
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              float4 o = reinterpret_cast<float4*>(h)[q];
-              float g0 = 1.f, g1 = 1.f, g2 = 1.f, g3 = 1.f;
-              if (p.gate) {
-                float4 gg = reinterpret_cast<const float4*>(p.gate + col)[q];
-                g0 = gg.x; g1 = gg.y; g2 = gg.z; g3 = gg.w;
-              }
-              o.x += g0 * v[4 * q];
-              o.y += g1 * v[4 * q + 1];
-              o.z += g2 * v[4 * q + 2];
-              o.w += g3 * v[4 * q + 3];
-              reinterpret_cast<float4*>(h)[q] = o;
+              o[q].x = fmaf(g[q].x, v[4 * q], o[q].x);
+              o[q].y = fmaf(g[q].y, v[4 * q + 1], o[q].y);
+              o[q].z = fmaf(g[q].z, v[4 * q + 2], o[q].z);
+              o[q].w = fmaf(g[q].w, v[4 * q + 3], o[q].w);
             }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) __stcs(h + q, o[q]);
           } else {
             if (p.epilogue == LP_EPI_STORE && p.bias) {
 #pragma unroll

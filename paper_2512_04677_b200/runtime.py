@@ -341,8 +341,12 @@ class Forward:
             L.call("lp_attention", C.byref(args), st)
             if self.probe:
                 self.probe("attention", "end", stream)
+            if self.probe:
+                self.probe("o_proj", "begin", stream)
             self._proj(st, self.att.data_ptr(), N, d, dw.wo[l], d, self.h.data_ptr(), d, L.EPI_RESID,
                        gate=mp(2))
+            if self.probe:
+                self.probe("o_proj", "end", stream)
             L.call("lp_norm_mod", self.h.data_ptr(), N, d, norm_mode, prof.eps, mp(3) or None, mp(4) or None,
                    self.xa.data_ptr(), ldt, st)
             if self.probe:
@@ -351,8 +355,12 @@ class Forward:
                        L.EPI_GELU if prof.act == "gelu_tanh" else L.EPI_RELU)
             if self.probe:
                 self.probe("ffn_up", "end", stream)
+            if self.probe:
+                self.probe("ffn_down", "begin", stream)
             self._proj(st, self.act.data_ptr(), N, f, dw.w2[l], d, self.h.data_ptr(), d, L.EPI_RESID,
                        gate=mp(5))
+            if self.probe:
+                self.probe("ffn_down", "end", stream)
         # head + flow step (denoiser.py:268, latent.py:140-147)
         if prof.adaln:
             L.call("lp_norm_mod", self.h.data_ptr(), N, d, 2, prof.eps, self.hmod.data_ptr(),
