@@ -145,19 +145,87 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args):
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "MEASURED_PEAKS.json"
+    except OSError:
+        return {}, None
+
+
+def probe_kernels(stages, run_block, stream):
+    """Eager per-kernel timing pass: CUDA events on the launch stream around
+    every tagged kernel of one more block."""
     import torch
 
-    import paper_2512_04677_b200 as lp
-    from paper_2512_04677_b200 import _lib as L
+    evs = {}
+
+    def probe(tag, phase, st):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(st or torch.cuda.current_stream())
+        evs.setdefault(tag, []).append(ev)
+
+    for st_ in stages:
+        st_.eager = True
+        st_.fw.probe = probe
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    run_block()
+    p1.record(stream)
+    torch.cuda.synchronize()
+    for st_ in stages:
+        st_.fw.probe = None
+        st_.eager = False
+    total = p0.elapsed_time(p1)
+    kern = {}
+    for tag, lst in evs.items():
+        durs = [lst[2 * i].elapsed_time(lst[2 * i + 1]) for i in range(len(lst) // 2)]
+        kern[tag] = {"launches": len(durs), "avg_ms": sum(durs) / len(durs), "sum_ms": sum(durs),
+                     "share": sum(durs) / total}
+    return kern, total
+
+
+def roofline(prof, kern, n_tok, n_kv):
+    """Roofline object for the dominant kernel (flash attention) plus the
+    per-GEMM achieved TFLOP/s (algorithmic FLOPs / CUDA-event duration)."""
+    peaks, src = _peaks()
+    peak_tf = peaks.get("bf16_tflops", 1590.0)
+    d, f = prof.model_dim, prof.ffn_dim
+    flops = {"attention": 4.0 * n_tok * n_kv * d, "qkv": 2.0 * n_tok * d * 3 * d, "o_proj": 2.0 * n_tok * d * d,
+             "ffn_up": 2.0 * n_tok * d * f, "ffn_down": 2.0 * n_tok * f * d}
+    for tag, fl in flops.items():
+        if tag in kern:
+            kern[tag]["flops_per_launch"] = fl
+            kern[tag]["tflops"] = fl / (kern[tag]["avg_ms"] / 1e3) / 1e12
+            kern[tag]["frac_of_peak"] = kern[tag]["tflops"] / peak_tf
+    if "attention" not in kern:
+        return None
+    ach = kern["attention"]["tflops"]
+    return {"bound": "tensor", "kernel": "attn_tc_kernel (tcgen05 flash attention, one layer, all heads)",
+            "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach / peak_tf, "traffic": TRAFFIC.get(
+                "attention"), "flops_per_launch": flops["attention"], "avg_launch_ms": kern["attention"]["avg_ms"],
+            "share_of_step": kern["attention"]["share"],
+            "peak_source": f"{src} bf16_tflops (burst)" if src else "fallback 1590 TFLOP/s"}
+
+
+# dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
+# `ncu --set full` capture (profiles/); None until captured.
+TRAFFIC = {}
+try:
+    TRAFFIC = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+except (OSError, ValueError):
+    TRAFFIC = {}
+
+
+def run_ours(args):
+    import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        from paper_2512_04677_b200 import tpp_dist
+        return run_dist(args, rank, world, local)
 
-        return tpp_dist.bench_main(args, rank, world, local)
+    import paper_2512_04677_b200 as lp
 
     dev = local
     torch.cuda.set_device(dev)
@@ -212,52 +280,14 @@ def run_ours(args):
     wall_e2e = time.perf_counter() - t0
     e2e_fps = FRAMES_PER_BLOCK_VIDEO * K / e2e_s
 
-    # ---- per-kernel timing pass (eager launches, CUDA events on the launch stream)
-    kern = {}
+    kern, probe_ms = {}, None
     if not args.no_probe:
-        evs = {}
-
-        def probe(tag, phase, stream):
-            st = stream or torch.cuda.current_stream()
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record(st)
-            evs.setdefault(tag, []).append(ev)
-
-        for st_ in pipe.stages.values():
-            st_.eager = True
-            st_.fw.probe = probe
-        b = base + K
-        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        p0.record(s)
-        pipe.submit(b, noise_dev[0])
-        p1.record(s)
-        torch.cuda.synchronize(dev)
-        for st_ in pipe.stages.values():
-            st_.fw.probe = None
-            st_.eager = False
-        probe_total = p0.elapsed_time(p1)
-        for tag, lst in evs.items():
-            durs = [lst[2 * i].elapsed_time(lst[2 * i + 1]) for i in range(len(lst) // 2)]
-            kern[tag] = {"launches": len(durs), "avg_ms": sum(durs) / len(durs), "sum_ms": sum(durs),
-                         "share": sum(durs) / probe_total}
-    d = prof.model_dim
-    att_flops = 4.0 * n_tok * n_kv_steady * d
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
+        kern, probe_ms = probe_kernels(list(pipe.stages.values()), lambda: pipe.submit(base + K, noise_dev[0]), s)
+    roof = roofline(prof, kern, n_tok, n_kv_steady)
+    peaks, _ = _peaks()
     peak_tf = peaks.get("bf16_tflops", 1590.0)
-    roof = None
-    if "attention" in kern:
-        ach = att_flops / (kern["attention"]["avg_ms"] / 1e3) / 1e12
-        roof = {"bound": "tensor", "kernel": "attn_tc_kernel (tcgen05 flash attention, per layer, all heads)",
-                "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach / peak_tf, "traffic": None,
-                "flops_per_launch": att_flops, "avg_launch_ms": kern["attention"]["avg_ms"],
-                "share_of_step": kern["attention"]["share"],
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "fallback 1590"}
     flops_block = T * prof.flops_per_forward(n_tok, n_kv_steady)
-    mfu = flops_block / dev_s * K / 1e12
+    ach = flops_block * K / dev_s / 1e12
     line = {
         "metric": METRIC, "value": fps, "unit": "FPS", "n_gpus": 1, "steps": K, "warmup": W,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -265,7 +295,9 @@ def run_ours(args):
         "config": {"workload": workload(args.config), "steps_T": T, "cache_L": Lc, "tokens_per_block": n_tok,
                    "n_kv_steady": n_kv_steady, "parallelism": "1 GPU, T steps sequential (TPP stages collapsed)",
                    "l2": "inputs (weights + KV rings) >> 126 MB L2; no flush needed",
-                   "block_latency_ms": ms_step, "achieved_tflops": mfu, "mfu_of_burst_peak": mfu / peak_tf},
+                   "block_latency_ms": ms_step, "achieved_tflops": ach, "frac_of_burst_peak": ach / peak_tf,
+                   "roofline_fps": FRAMES_PER_BLOCK_VIDEO / (flops_block / (peak_tf * 1e12)),
+                   "probe_block_ms": probe_ms},
         "e2e": {"value": e2e_fps, "unit": "FPS", "h2d_bytes_per_step": 3 * lat * 4,
                 "d2h_bytes_per_step": 3 * lat * 4, "wall_s": wall_e2e},
         "gpu_launches": launches_per_block * K,
@@ -277,6 +309,120 @@ def run_ours(args):
         except Exception as exc:  # noqa: BLE001
             line["cpu_baseline"] = {"error": str(exc)}
     print(json.dumps(line), flush=True)
+
+
+def run_dist(args, rank, world, local):
+    """N > 1: one process per GPU, TPP stage groups (tpp_dist.DistTPP); the
+    pipeline(s) stream K blocks, timed per rank with CUDA events on the
+    rank's stream between barriers; the max over ranks is the job time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_04677_b200 as lp
+    from paper_2512_04677_b200 import tpp_dist
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    prof = profile_for(args.config)
+    T, Lc = 4, 4
+    cfg = lp.EngineConfig(mode="tpp", steps=T, cache_capacity=Lc, frames_per_block=3, profile=prof,
+                          precision="bf16", devices=(local,), device_inputs=True, blocks=1 << 20,
+                          link_capacity=2, link_timeout_s=600.0)
+    run = tpp_dist.DistTPP(cfg, transport="ipc", device=local)
+    role = run.role
+    be = run.backend
+    n_tok = 3 * prof.tokens_per_frame
+    lat = prof.latent_dim
+    K, W = args.steps, max(args.warmup, 3)
+    g = torch.Generator(device=f"cuda:{local}").manual_seed(11 + role.pipe)
+    noise_dev = torch.randn((W + K + 1, 3, lat), generator=g, device=f"cuda:{local}")
+    out_dev = torch.empty((3, lat), device=f"cuda:{local}")
+    for i in range(W):
+        run.step(i, noise=noise_dev[i], out=out_dev if i else None)
+    run.finish()
+    dist.barrier()
+    torch.cuda.synchronize(local)
+    n_kv_steady = prof.tokens_per_frame + Lc * n_tok + n_tok
+    s = be.stream
+    ends = []
+    e0 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize(local)
+        e0.record(s)
+        for i in range(W, W + K):
+            run.step(i, noise=noise_dev[i], out=out_dev)
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(s)
+            ends.append(ev)
+        torch.cuda.synchronize(local)
+        run.finish()
+        dist.barrier()
+    el = e0.elapsed_time(ends[-1]) / 1e3
+    t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    job_s = float(t.item())
+    fps = FRAMES_PER_BLOCK_VIDEO * K * role.n_pipes / job_s
+    steady = None
+    if role.last and K >= 3:
+        gaps = [ends[k - 1].elapsed_time(ends[k]) for k in range(1, K)]
+        steady = FRAMES_PER_BLOCK_VIDEO / (statistics.median(gaps) / 1e3)
+
+    # e2e: pinned host noise in on the first rank, pinned host latent out on the last
+    host_in = torch.randn((K, 3, lat)).pin_memory()
+    host_out = torch.empty((K, 3, lat)).pin_memory()
+    base = W + K
+    dist.barrier()
+    torch.cuda.synchronize(local)
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(s)
+    for k in range(K):
+        run.step(base + k, noise=host_in[k], out=host_out[k])
+    e3.record(s)
+    torch.cuda.synchronize(local)
+    run.finish()
+    t = torch.tensor([e2.elapsed_time(e3) / 1e3], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_fps = FRAMES_PER_BLOCK_VIDEO * K * role.n_pipes / float(t.item())
+
+    kern = {}
+    if not args.no_probe:
+        kern, _ = probe_kernels(be.stages, lambda: run.step(base + K, noise=noise_dev[W + K], out=out_dev), s)
+        run.finish()
+    roof = roofline(prof, kern, n_tok, n_kv_steady)
+    steady_t = torch.tensor([steady or 0.0], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(steady_t, op=dist.ReduceOp.MAX)
+    launches = torch.tensor([sum(st.fw.kernels_per_forward() for st in be.stages) * K], dtype=torch.int64,
+                            device=f"cuda:{local}")
+    dist.all_reduce(launches)
+    peaks, _ = _peaks()
+    peak_tf = peaks.get("bf16_tflops", 1590.0)
+    flops_block = T * prof.flops_per_forward(n_tok, n_kv_steady)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": fps, "unit": "FPS", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": 1e3 * job_s / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (device-RNG random-init weights, N(0,1) noise blocks)",
+            "config": {"workload": workload(args.config), "steps_T": T, "cache_L": Lc, "tokens_per_block": n_tok,
+                       "n_kv_steady": n_kv_steady,
+                       "parallelism": f"TPP: {role.n_pipes} pipeline(s) x {len(role.ranks)} stage GPUs "
+                                      f"(steps per GPU {[r.steps for r in run.roles[:len(role.ranks)]]}), "
+                                      "latents over NVLink P2P (CUDA IPC links)",
+                       "l2": "inputs (weights + KV rings) >> 126 MB L2; no flush needed",
+                       "steady_fps_last_stage": float(steady_t.item()) * role.n_pipes,
+                       "timed_region": "K blocks incl. pipeline fill (barrier-bracketed)",
+                       "achieved_tflops": flops_block * K * role.n_pipes / job_s / 1e12,
+                       "roofline_fps": FRAMES_PER_BLOCK_VIDEO * len(role.ranks) * role.n_pipes
+                       / (flops_block / (peak_tf * 1e12))},
+            "e2e": {"value": e2e_fps, "unit": "FPS", "h2d_bytes_per_step": 3 * lat * 4 * role.n_pipes,
+                    "d2h_bytes_per_step": 3 * lat * 4 * role.n_pipes},
+            "gpu_launches": int(launches.item()),
+            "roofline": roof, "kernels": kern, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    run.close()
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def main():

@@ -248,6 +248,23 @@ LP_API int lp_link_recv(const void* src_slot, void* dst, int64_t bytes, volatile
                  volatile const uint32_t* abort_word, uint64_t timeout_ns,
                  int32_t* status_out, void* stream);
 
+/* Publish `value` into a (possibly peer-mapped) flag with a system-scope
+   release after all prior work on `stream` (the "ready"/"sink posted" half
+   of a link, engine.py:369 / :477-478).                                    */
+LP_API int lp_signal(volatile uint32_t* flag, uint32_t value, void* stream);
+/* Stream-ordered bounded wait until *flag >= target (engine.py:379, :439);
+   *status_out = 0, LP_EABORT or LP_ETIMEOUT (status_out may be NULL).       */
+LP_API int lp_wait(volatile const uint32_t* flag, uint32_t target, volatile const uint32_t* abort_word,
+            uint64_t timeout_ns, int32_t* status_out, void* stream);
+
+/* CUDA IPC for the one-process-per-GPU TPP runtime: export the allocation
+   containing dev_ptr as a 64-byte handle plus the pointer's offset inside it,
+   and map a peer's handle into this process (peer access over NVLink is
+   enabled lazily).  lp_ipc_close takes the mapped BASE (ptr - offset).      */
+LP_API int lp_ipc_handle(const void* dev_ptr, uint8_t* handle_out, int64_t* offset_out);
+LP_API int lp_ipc_open(const uint8_t* handle, int64_t offset, void** ptr_out);
+LP_API int lp_ipc_close(void* mapped_base);
+
 #ifdef __cplusplus
 }
 #endif

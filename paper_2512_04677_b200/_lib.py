@@ -83,6 +83,11 @@ _SIGS = {
     "lp_randn_bf16": ([vp, i64, u64, u64, C.c_float, vp], C.c_int),
     "lp_link_send": ([vp, vp, i64, vp, vp, u32, C.c_int, vp, u64, vp], C.c_int),
     "lp_link_recv": ([vp, vp, i64, vp, vp, u32, vp, u64, vp, vp], C.c_int),
+    "lp_signal": ([vp, u32, vp], C.c_int),
+    "lp_wait": ([vp, u32, vp, u64, vp, vp], C.c_int),
+    "lp_ipc_handle": ([vp, vp, C.POINTER(i64)], C.c_int),
+    "lp_ipc_open": ([vp, i64, C.POINTER(vp)], C.c_int),
+    "lp_ipc_close": ([vp], C.c_int),
 }
 
 

@@ -40,6 +40,12 @@ int link_send(const void*, void*, int64_t, volatile uint32_t*, const volatile ui
 int link_recv(const void*, void*, int64_t, const volatile uint32_t*, volatile uint32_t*, uint32_t,
               const volatile uint32_t*, uint64_t, int32_t*, cudaStream_t);
 
+int signal(volatile uint32_t*, uint32_t, cudaStream_t);
+int wait(const volatile uint32_t*, uint32_t, const volatile uint32_t*, uint64_t, int32_t*, cudaStream_t);
+int ipc_handle(const void*, uint8_t*, int64_t*);
+int ipc_open(const uint8_t*, int64_t, void**);
+int ipc_close(void*);
+
 int preload_links();
 int preload_f32();
 int preload_rows();
@@ -174,5 +180,20 @@ int lp_link_recv(const void* src_slot, void* dst, int64_t bytes, volatile const 
   return link_recv(src_slot, dst, bytes, ready_flag, free_flag, seq, abort_word, timeout_ns, status_out,
                    S(stream));
 }
+
+int lp_signal(volatile uint32_t* flag, uint32_t value, void* stream) { return signal(flag, value, S(stream)); }
+
+int lp_wait(volatile const uint32_t* flag, uint32_t target, volatile const uint32_t* abort_word, uint64_t timeout_ns,
+            int32_t* status_out, void* stream) {
+  return wait(flag, target, abort_word, timeout_ns, status_out, S(stream));
+}
+
+int lp_ipc_handle(const void* dev_ptr, uint8_t* handle_out, int64_t* offset_out) {
+  return ipc_handle(dev_ptr, handle_out, offset_out);
+}
+
+int lp_ipc_open(const uint8_t* handle, int64_t offset, void** ptr_out) { return ipc_open(handle, offset, ptr_out); }
+
+int lp_ipc_close(void* mapped_base) { return ipc_close(mapped_base); }
 
 }  // extern "C"

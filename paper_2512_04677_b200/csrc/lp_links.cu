@@ -10,6 +10,9 @@
 // Sequence numbers enforce the reference's FIFO invariant (engine.py:360-363,
 // :383-387); waits are bounded and poll an abort word so a failed stage
 // unwinds its peers (engine.py:425-429, :499-506).
+#include <cuda.h>
+#include <string.h>
+
 #include "lp_common.cuh"
 
 namespace lp {
@@ -79,12 +82,25 @@ __global__ void link_recv_kernel(const uint4* src, uint4* __restrict__ dst, int6
   }
 }
 
+__global__ void signal_kernel(volatile uint32_t* flag, uint32_t value) {
+  __threadfence_system();
+  st_release_sys(flag, value);
+}
+
+__global__ void wait_kernel(const volatile uint32_t* flag, uint32_t target, const volatile uint32_t* abort_word,
+                            uint64_t timeout_ns, int32_t* status) {
+  int st = wait_geq(flag, target, abort_word, timeout_ns);
+  if (status) *status = st;
+}
+
 // Force-load the link kernels: with lazy module loading, the first launch of
 // a kernel while another stream's waiter spins can stall on the loader.
 int preload_links() {
   cudaFuncAttributes a;
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, link_send_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, link_recv_kernel));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, signal_kernel));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, wait_kernel));
   return LP_OK;
 }
 
@@ -105,6 +121,62 @@ int link_recv(const void* src, void* dst, int64_t bytes, const volatile uint32_t
   link_recv_kernel<<<1, 1024, 0, st>>>((const uint4*)src, (uint4*)dst, bytes / 16, ready, freef, seq, abort_word,
                                        timeout_ns, status);
   return launch_status("link_recv");
+}
+
+int signal(volatile uint32_t* flag, uint32_t value, cudaStream_t st) {
+  LP_CHECK_ARG(flag != nullptr, "lp_signal: null flag");
+  signal_kernel<<<1, 1, 0, st>>>(flag, value);
+  return launch_status("signal");
+}
+
+int wait(const volatile uint32_t* flag, uint32_t target, const volatile uint32_t* abort_word, uint64_t timeout_ns,
+         int32_t* status, cudaStream_t st) {
+  LP_CHECK_ARG(flag != nullptr, "lp_wait: null flag");
+  wait_kernel<<<1, 1, 0, st>>>(flag, target, abort_word, timeout_ns, status);
+  return launch_status("wait");
+}
+
+// ---- CUDA IPC: export / map device allocations across processes ----------
+// A torch tensor's data pointer is usually interior to a caching-allocator
+// segment; the handle names the whole allocation, so the exporter also
+// reports the offset of the pointer inside it (cuMemGetAddressRange).
+using GetRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+static GetRangeFn g_range = nullptr;
+
+int ipc_handle(const void* ptr, uint8_t* handle64, int64_t* offset) {
+  LP_CHECK_ARG(ptr && handle64 && offset, "lp_ipc_handle: null argument");
+  if (!g_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    LP_CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(LP_ECUDA, "cuMemGetAddressRange not available");
+    g_range = reinterpret_cast<GetRangeFn>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  CUresult r = g_range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr));
+  if (r != CUDA_SUCCESS) return fail(LP_ECUDA, "cuMemGetAddressRange failed: " + std::to_string((int)r));
+  cudaIpcMemHandle_t h;
+  LP_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  memcpy(handle64, &h, sizeof(h));
+  *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(ptr) - base);
+  return LP_OK;
+}
+
+int ipc_open(const uint8_t* handle64, int64_t offset, void** out) {
+  LP_CHECK_ARG(handle64 && out, "lp_ipc_open: null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  void* base = nullptr;
+  LP_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *out = static_cast<uint8_t*>(base) + offset;
+  return LP_OK;
+}
+
+int ipc_close(void* base) {
+  LP_CHECK_ARG(base != nullptr, "lp_ipc_close: null argument");
+  LP_CUDA_TRY(cudaIpcCloseMemHandle(base));
+  return LP_OK;
 }
 
 }  // namespace lp

@@ -1,0 +1,40 @@
+"""One-process-per-GPU TPP on the device: ranks exchange CUDA IPC handles
+(gloo), latents cross ranks through IpcLink (device-initiated copies +
+release/acquire flags), the sink is broadcast once after block 0.  The box
+has one GPU, so the ranks share cuda:0 (same IPC + flag protocol as across
+NVLink peers).  Results must equal the single-process sequential run
+bitwise (reference tests/test_acceptance.py:60-83)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2512_04677_b200 as lp
+
+from test_tpp_dist_cpu import META, launch
+from dist_worker import wan_small
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("nproc,name", [(2, "c1"), (4, "c1_sigma")])
+def test_ipc_tpp_fp32_equals_sequential(tmp_path, nproc, name):
+    kw = dict(META[name]["kw"])
+    out = tmp_path / "res"
+    launch(nproc, "gpu", out, dict(kw, link_timeout_s=60.0), timeout=600)
+    got = np.load(f"{out}.0.npy")
+    seq = lp.run_sequential(lp.EngineConfig(mode="sequential", **kw))
+    assert got.tobytes() == np.stack([b.values for b in seq.blocks]).tobytes()
+    rec = json.load(open(f"{out}.0"))
+    assert rec["nfe"] == META[name]["nfe"]
+
+
+def test_ipc_tpp_bf16_wan_equals_sequential(tmp_path):
+    kw = dict(steps=4, blocks=4, cache_capacity=2)
+    out = tmp_path / "res"
+    launch(2, "gpu", out, dict(kw, precision="bf16", profile="wan_small", link_timeout_s=60.0), timeout=600)
+    got = np.load(f"{out}.0.npy")
+    seq = lp.run_sequential(lp.EngineConfig(mode="sequential", precision="bf16", profile=wan_small(), **kw))
+    assert got.tobytes() == np.stack([b.values for b in seq.blocks]).tobytes()
