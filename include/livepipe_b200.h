@@ -159,7 +159,14 @@ typedef struct lp_attn_args {
   const lp_block_desc* desc;
   int32_t arena_rows;     /* rows in the arena (bounds for TMA)             */
   int32_t n_kv_max;       /* host-known upper bound of visible keys         */
+  void* workspace;        /* LP_BF16: partials of KV-split work units (the
+                             tail of the grid is split to fill the last wave;
+                             NULL or too small => no splitting)             */
+  int64_t workspace_bytes;
 } lp_attn_args;
+/* Bytes of lp_attn_args.workspace the tcgen05 attention uses for n_q queries
+   and n_heads heads on this device (0 when no unit is split).               */
+LP_API int lp_attention_workspace(int n_q, int n_heads, int head_dim, int64_t* bytes_out);
 LP_API int lp_attention(const lp_attn_args* args, void* stream);
 /* SIMT reference attention for either dtype (validation tool: same math,
    reference order; used by tests to check the tcgen05 kernel on identical

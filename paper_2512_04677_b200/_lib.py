@@ -57,7 +57,7 @@ class GemmArgs(C.Structure):
 class AttnArgs(C.Structure):
     _fields_ = [("dtype", i32), ("n_q", i32), ("n_heads", i32), ("head_dim", i32), ("scale", f32),
                 ("q", vp), ("k_arena", vp), ("v_arena", vp), ("out", vp), ("desc", vp),
-                ("arena_rows", i32), ("n_kv_max", i32)]
+                ("arena_rows", i32), ("n_kv_max", i32), ("workspace", vp), ("workspace_bytes", i64)]
 
 
 _SIGS = {
@@ -69,6 +69,7 @@ _SIGS = {
     "lp_qkv_post": ([vp, C.c_int, C.POINTER(QkvEpi), C.c_int, vp], C.c_int),
     "lp_attention": ([C.POINTER(AttnArgs), vp], C.c_int),
     "lp_attention_simt": ([C.POINTER(AttnArgs), vp], C.c_int),
+    "lp_attention_workspace": ([C.c_int, C.c_int, C.c_int, C.POINTER(i64)], C.c_int),
     "lp_cond_row": ([vp, C.c_int, vp, vp, C.c_int, vp, vp, C.c_int, vp, vp, C.c_int, vp], C.c_int),
     "lp_add_row": ([vp, vp, vp, C.c_int, C.c_int, vp], C.c_int),
     "lp_norm_mod": ([vp, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp, vp, C.c_int, vp], C.c_int),

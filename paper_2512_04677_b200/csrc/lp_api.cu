@@ -23,6 +23,7 @@ int qkv_post(const float* qkv, int m, const lp_qkv_epi& e, int out_dtype, cudaSt
 int attention_simt(const lp_attn_args* a, int n_kv_max, cudaStream_t st);
 int gemm_tc(const lp_gemm_args* a, cudaStream_t st);
 int attention_tc(const lp_attn_args* a, cudaStream_t st);
+int64_t attention_workspace_bytes(int n_q, int n_heads);
 int cond_row(const float*, int, const float*, const float*, int, const float*, const float*, int, const float*,
              float*, int, cudaStream_t);
 int add_row(const float*, const float*, float*, int, int, cudaStream_t);
@@ -108,6 +109,13 @@ int lp_attention(const lp_attn_args* a, void* stream) {
   if (a->dtype == LP_BF16) return attention_tc(a, S(stream));
   LP_CHECK_ARG(a->dtype == LP_F32, "lp_attention: dtype");
   return attention_simt(a, a->n_kv_max, S(stream));
+}
+
+int lp_attention_workspace(int n_q, int n_heads, int head_dim, int64_t* bytes_out) {
+  LP_CHECK_ARG(bytes_out != nullptr, "lp_attention_workspace: null argument");
+  LP_CHECK_ARG(num_sms() > 0, "lp_init() must be called before lp_attention_workspace");
+  *bytes_out = head_dim == 128 ? attention_workspace_bytes(n_q, n_heads) : 0;
+  return LP_OK;
 }
 
 int lp_attention_simt(const lp_attn_args* a, void* stream) {

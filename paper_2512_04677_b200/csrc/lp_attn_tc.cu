@@ -1,8 +1,13 @@
 // tcgen05 flash attention over the RSFM key set [sink | history ring | current]
 // (denoiser.py:246-264, _attend_head :152-158, softmax numerics.py:67-78).
 //
-// One CTA per (256 queries, head): two 128-row Q tiles (A, B) share every
-// K/V tile.  Head dim 128, bf16 Q/K/V, fp32 S/O in TMEM, online softmax in
+// One CTA per work unit = (256 queries, head[, KV range]): two 128-row Q
+// tiles (A, B) share every K/V tile.  Wave quantisation: the host orders the
+// units regular-first and splits the last few (the ragged query tail of each
+// head plus as many regular units as the makespan model asks for) into S
+// KV-range pieces whose (O, m, l) partials are merged by attn_combine_kernel
+// in a fixed order (deterministic).  A unit whose tile B lies wholly past
+// n_q skips B's MMAs and softmax.  Head dim 128, bf16 Q/K/V, fp32 S/O in TMEM, online softmax in
 // fp32.  KV tiles of 128 keys walk the descriptor's segments in reference
 // order (sink, oldest -> newest history, current); the ragged tail of a
 // segment is masked to -inf, so segments need no padding and nothing is
@@ -17,13 +22,22 @@
 //   warps 2-5   softmax warpgroup A, warps 6-9 softmax warpgroup B: thread =
 //               query row; S row from TMEM in one pass, exp2 with a lazily
 //               updated running max (O is rescaled in TMEM only when the max
-//               grows by more than 2^8), P written back to TMEM as bf16 over
+//               grows by more than 2^8; 1/4 of the exponentials run as a
+//               degree-3 polynomial on the FMA pipe so MUFU is not the
+//               co-bottleneck with the tensor core), P written back to TMEM as bf16 over
 //               its own S columns and consumed from TMEM by the P.V MMA
 //               (A-operand-in-TMEM form), O / l -> bf16 at the end
 //
 // TMEM columns: S_A|P_A [0,128)  S_B|P_B [128,256)  O_A [256,384)  O_B [384,512).
 // In-order completion of one thread's tcgen05.mma stream makes the S(j+1)
 // write after P(j).V safe, and s_full(j) imply P(j-1).V done.
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <queue>
+#include <tuple>
+#include <vector>
+
 #include "lp_common.cuh"
 #include "lp_sm100.cuh"
 #include "lp_tma.cuh"
@@ -47,6 +61,7 @@ struct AttnSmem {
   static constexpr int BAR_OFF = V_OFF + 2 * AT_TILE_BYTES;
   static constexpr int SEG_OFF = BAR_OFF + 256;
   static constexpr int TOTAL = SEG_OFF + 2 * LP_MAX_SEG * 4 + 16 + 1024;
+  static_assert(2 * LP_MAX_SEG * 4 + 16 >= 2 * LP_MAX_SEG * 4 + 3 * 4, "segment scratch");
 };
 
 struct AttnParams {
@@ -55,7 +70,87 @@ struct AttnParams {
   __nv_bfloat16* out;
   int64_t ldo;
   const lp_block_desc* desc;
+  // work decomposition (see AttnPlan)
+  int pairs;      // 256-query units per head
+  int reg_pairs;  // units per head whose both tiles hold valid rows
+  int n_whole;    // leading units run whole (grid prefix)
+  int split;      // KV pieces per split unit
+  float* part_o;  // [piece][256][128] unnormalised O of split units
+  float* part_ml; // [piece][256][2]   (running max in log2 units, row sum)
 };
+
+// Unit u -> (head, pair): regular units (both Q tiles valid) first, head-major
+// so concurrently running CTAs share K/V in L2, then the ragged tail unit of
+// every head.
+__device__ __forceinline__ void unit_coords(const AttnParams& p, int u, int& head, int& pair) {
+  const int n_reg = p.reg_pairs * p.n_heads;
+  if (u < n_reg) {
+    head = u / p.reg_pairs;
+    pair = u % p.reg_pairs;
+  } else {
+    head = u - n_reg;
+    pair = p.pairs - 1;
+  }
+}
+
+// packed fp32x2 helpers (FFMA2 / FADD2 on sm_100)
+__device__ __forceinline__ uint64_t f32x2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void unpack_f32x2(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2_rm(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// Packed version of ex2_poly (below) for a pair.
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t xv) {
+  float x0, x1;
+  unpack_f32x2(xv, x0, x1);
+  xv = f32x2(fmaxf(x0, -127.0f), fmaxf(x1, -127.0f));
+  const uint64_t magic = f32x2(12582912.0f, 12582912.0f);
+  const uint64_t t = fadd2_rm(xv, magic);
+  const uint64_t f = fsub2(xv, fsub2(t, magic));
+  uint64_t q = ffma2(f32x2(0.07706641f, 0.07706641f), f, f32x2(0.2276457f, 0.2276457f));
+  q = ffma2(q, f, f32x2(0.69511662f, 0.69511662f));
+  q = ffma2(q, f, f32x2(1.0f, 1.0f));
+  float q0, q1, t0, t1;
+  unpack_f32x2(q, q0, q1);
+  unpack_f32x2(t, t0, t1);
+  return f32x2(__int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23)),
+               __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23)));
+}
+
+// 2^x for x <= 8 on the FMA pipe: Cody-Waite split x = j + f, degree-3
+// minimax polynomial for 2^f on [0, 1) (max rel. error 8.6e-5, far below the
+// bf16 rounding of P), exponent added as an integer.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -127.0f);
+  const float t = __fadd_rd(x, 12582912.0f);  // 1.5 * 2^23: floor(x) lands in the low mantissa bits
+  const float f = __fsub_rn(x, __fsub_rn(t, 12582912.0f));
+  const float q = fmaf(fmaf(fmaf(0.07706641f, f, 0.2276457f), f, 0.69511662f), f, 1.0f);
+  return __int_as_float(__float_as_int(q) + (__float_as_int(t) << 23));
+}
 
 // Walks the KV tiles of the descriptor's segments in order.
 struct TileCursor {
@@ -65,6 +160,9 @@ struct TileCursor {
   __device__ void init(const int* r, const int* l, int n) {
     row = r; len = l; n_seg = n; seg = 0; off = 0;
     while (seg < n_seg && len[seg] == 0) ++seg;
+  }
+  __device__ void skip(int tiles) {
+    for (int i = 0; i < tiles; ++i) next();
   }
   __device__ int cur_row() const { return row[seg] + off; }
   __device__ int cur_valid() const { return min(AT_N, len[seg] - off); }
@@ -114,8 +212,18 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   int* n_seg_s = seg_len + LP_MAX_SEG;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int head = blockIdx.y;
-  const int q0 = blockIdx.x * (2 * AT_M);
+  int unit, piece = -1;
+  if ((int)blockIdx.x < p.n_whole) {
+    unit = blockIdx.x;
+  } else {
+    const int v = blockIdx.x - p.n_whole;
+    unit = p.n_whole + v / p.split;
+    piece = v % p.split;
+  }
+  int head, pair;
+  unit_coords(p, unit, head, pair);
+  const int q0 = pair * (2 * AT_M);
+  const bool two = q0 + AT_M < p.n_q;  // tile B holds valid rows
 
   const int nseg = min(p.desc->n_seg, LP_MAX_SEG);
   for (int s = threadIdx.x; s < nseg; s += blockDim.x) {
@@ -126,7 +234,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     int nt = 0;
     for (int s = 0; s < nseg; ++s) nt += (p.desc->seg_len[s] + AT_N - 1) / AT_N;
     n_seg_s[0] = nseg;
-    n_seg_s[1] = nt;
+    // this CTA's KV tile range: all tiles, or piece `piece` of `split`
+    const int t0 = piece < 0 ? 0 : (int)((int64_t)nt * piece / p.split);
+    const int t1 = piece < 0 ? nt : (int)((int64_t)nt * (piece + 1) / p.split);
+    n_seg_s[1] = t1 - t0;
+    n_seg_s[2] = t0;
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -150,21 +262,23 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int n_tiles = n_seg_s[1];
+  const int t_first = n_seg_s[2];
   const int col0 = head * AT_D;
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     if (elect_one()) {
       uint8_t* sq = smem + AttnSmem::Q_OFF;
-      mbar_arrive_expect_tx(q_full, 2 * AT_TILE_BYTES);
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
+      mbar_arrive_expect_tx(q_full, (two ? 2 : 1) * AT_TILE_BYTES);
+      for (int t = 0; t < (two ? 2 : 1); ++t) {
         tma_load_2d(sq + t * AT_TILE_BYTES, &tmQ, q_full, col0, q0 + t * AT_M);
         tma_load_2d(sq + t * AT_TILE_BYTES + AT_HALF, &tmQ, q_full, col0 + 64, q0 + t * AT_M);
       }
       TileCursor ck, cv;
       ck.init(seg_row, seg_len, n_seg_s[0]);
       cv.init(seg_row, seg_len, n_seg_s[0]);
+      ck.skip(t_first);
+      cv.skip(t_first);
       const uint64_t pol = l2_policy_evict_last();
       for (int t = 0; t <= n_tiles; ++t) {
         if (t < n_tiles) {
@@ -217,8 +331,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       if (elect_one()) {
         issue_s(0, 0);
         mma_commit(&s_full[0]);
-        issue_s(0, 1);
-        mma_commit(&s_full[1]);
+        if (two) {
+          issue_s(0, 1);
+          mma_commit(&s_full[1]);
+        }
         mma_commit(&k_empty[0]);
       }
       __syncwarp();
@@ -236,21 +352,27 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           issue_s(j + 1, 0);
           mma_commit(&s_full[0]);
         }
-      }
-      __syncwarp();
-      // tile B: P_B(j) V_j, then S_B(j+1)
-      mbar_wait(&p_full[1], j & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        issue_pv(j, 1);
-        mma_commit(&v_empty[j & 1]);
-        if (more) {
-          issue_s(j + 1, 1);
-          mma_commit(&s_full[1]);
-          mma_commit(&k_empty[(j + 1) & 1]);
+        if (!two) {
+          mma_commit(&v_empty[j & 1]);
+          if (more) mma_commit(&k_empty[(j + 1) & 1]);
         }
       }
       __syncwarp();
+      if (two) {
+        // tile B: P_B(j) V_j, then S_B(j+1)
+        mbar_wait(&p_full[1], j & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          issue_pv(j, 1);
+          mma_commit(&v_empty[j & 1]);
+          if (more) {
+            issue_s(j + 1, 1);
+            mma_commit(&s_full[1]);
+            mma_commit(&k_empty[(j + 1) & 1]);
+          }
+        }
+        __syncwarp();
+      }
     }
     if (elect_one()) mma_commit(o_done);
     __syncwarp();
@@ -266,7 +388,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     float m_run = -INFINITY, l_run = 0.0f;
     TileCursor cs;
     cs.init(seg_row, seg_len, n_seg_s[0]);
-    for (int j = 0; j < n_tiles; ++j, cs.next()) {
+    cs.skip(t_first);
+    const bool active = x == 0 || two;
+    for (int j = 0; j < (active ? n_tiles : 0); ++j, cs.next()) {
       const int nvalid = cs.cur_valid();
       mbar_wait(&s_full[x], j & 1);
       tc_fence_after();
@@ -297,20 +421,38 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           m_run = m_tile;
         }
       }
-      // p = 2^(s*scale*log2e - m), packed to bf16 pairs in key order
-      float rs0 = 0.f, rs1 = 0.f;
-      uint32_t pk[64];
+      // p = 2^(s*scale*log2e - m), packed to bf16 pairs in key order.
+      // Pairs go through the packed fp32x2 FMA pipe (FFMA2/FADD2); 3 of
+      // every 8 pairs take the polynomial exp2, the rest MUFU.EX2.
+      const uint64_t sc2 = f32x2(sc, sc), nm2 = f32x2(-m_run, -m_run);
+      uint64_t rs2a = f32x2(0.f, 0.f), rs2b = rs2a;
+      uint32_t* pk = s;  // packed P overwrites the consumed front of s in place
 #pragma unroll
       for (int i = 0; i < 128; i += 2) {
-        const float e0 = ex2(fmaf(__uint_as_float(s[i]), sc, -m_run));
-        const float e1 = ex2(fmaf(__uint_as_float(s[i + 1]), sc, -m_run));
-        rs0 += e0;
-        rs1 += e1;
+        const bool poly = ((i >> 1) & 7) >= 5;
+        const uint64_t a = ffma2(f32x2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sc2, nm2);
+        uint64_t e;
+        if (poly) {
+          e = ex2_poly2(a);
+        } else {
+          float a0, a1;
+          unpack_f32x2(a, a0, a1);
+          e = f32x2(ex2(a0), ex2(a1));
+        }
+        if ((i >> 1) & 1)
+          rs2b = fadd2(rs2b, e);
+        else
+          rs2a = fadd2(rs2a, e);
+        float e0, e1;
+        unpack_f32x2(e, e0, e1);
         pk[i / 2] = pack_bf16(e0, e1);
       }
-      l_run = l_run * alpha + (rs0 + rs1);
-      tmem_st32_x(t_s + 0, &pk[0]);
-      tmem_st32_x(t_s + 32, &pk[32]);
+      float r0, r1, r2, r3;
+      unpack_f32x2(rs2a, r0, r1);
+      unpack_f32x2(rs2b, r2, r3);
+      l_run = l_run * alpha + ((r0 + r1) + (r2 + r3));
+      tmem_st32_x(t_s + 0, &s[0]);
+      tmem_st32_x(t_s + 32, &s[32]);
       if (rescale) {
         // P(j-1).V is complete (implied by s_full(j)); O_x is idle until p_full(j)
 #pragma unroll 1
@@ -328,11 +470,33 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[x]);
     }
-    // epilogue: O / l -> bf16
+    // epilogue: O / l -> bf16 (whole unit) or unnormalised (O, m, l) partials
+    if (active) {
     mbar_wait(o_done, 0);
     tc_fence_after();
-    const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
     const int row = q0 + x * AT_M + r;
+    if (piece >= 0) {
+      const int64_t slot = (int64_t)(blockIdx.x - p.n_whole) * (2 * AT_M) + x * AT_M + r;
+      float* po = p.part_o + slot * AT_D;
+#pragma unroll 1
+      for (int c0 = 0; c0 < AT_D; c0 += 32) {
+        uint32_t v[32];
+        if (n_tiles > 0) {
+          tmem_ld32(t_o + c0, v);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0u;
+        }
+        float4* o = reinterpret_cast<float4*>(po + c0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          o[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                             __uint_as_float(v[4 * q + 3]));
+      }
+      reinterpret_cast<float2*>(p.part_ml)[slot] = make_float2(n_tiles > 0 ? m_run : -INFINITY, l_run);
+    } else {
+    const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
 #pragma unroll 1
     for (int c0 = 0; c0 < AT_D; c0 += 32) {
       uint32_t v[32];
@@ -348,6 +512,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                             pack_bf16(__uint_as_float(v[8 * q + 6]) * inv_l, __uint_as_float(v[8 * q + 7]) * inv_l));
       }
     }
+    }
+    }
   }
 
   tc_fence_before();
@@ -358,10 +524,118 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   }
 }
 
+// Merge the KV-range partials of the split units in piece order:
+// O = sum_s 2^(m_s - m) O_s / sum_s 2^(m_s - m) l_s (one warp per query row).
+__global__ void __launch_bounds__(256) attn_combine_kernel(const AttnParams p) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  const int k = warp / (2 * AT_M);  // split unit
+  const int r = warp % (2 * AT_M);  // row within the unit
+  const int n_units = p.pairs * p.n_heads;
+  if (p.n_whole + k >= n_units) return;
+  int head, pair;
+  unit_coords(p, p.n_whole + k, head, pair);
+  const int row = pair * (2 * AT_M) + r;
+  if (row >= p.n_q) return;
+  const float2* ml = reinterpret_cast<const float2*>(p.part_ml);
+  const int64_t base = (int64_t)k * p.split * (2 * AT_M) + r;
+  float m = -INFINITY;
+  for (int s = 0; s < p.split; ++s) m = fmaxf(m, ml[base + (int64_t)s * (2 * AT_M)].x);
+  float l = 0.f;
+  float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s = 0; s < p.split; ++s) {
+    const int64_t slot = base + (int64_t)s * (2 * AT_M);
+    const float2 v = ml[slot];
+    const float w = v.x == -INFINITY ? 0.f : exp2f(v.x - m);
+    l = fmaf(w, v.y, l);
+    const float4 x = reinterpret_cast<const float4*>(p.part_o + slot * AT_D)[lane];
+    o.x = fmaf(w, x.x, o.x);
+    o.y = fmaf(w, x.y, o.y);
+    o.z = fmaf(w, x.z, o.z);
+    o.w = fmaf(w, x.w, o.w);
+  }
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  uint2* dst = reinterpret_cast<uint2*>(p.out + (int64_t)row * p.ldo + head * AT_D + lane * 4);
+  *dst = make_uint2(pack_bf16(o.x * inv, o.y * inv), pack_bf16(o.z * inv, o.w * inv));
+}
+
 int preload_attn_tc() {
   cudaFuncAttributes a;
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_tc_kernel));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_combine_kernel));
   return LP_OK;
+}
+
+// Work decomposition for (n_q, n_heads) on `sms` SMs.  Units are 256-query
+// pairs of one head; a pair whose second tile is empty costs ~0.6.  The last
+// n_split units (all ragged ones first in line) are cut into `split`
+// KV-range pieces.  (n_split, split) minimise the makespan of in-order
+// dispatch to the earliest-free SM (the hardware block scheduler), with a
+// small fixed cost per CTA and for the combine pass.
+struct AttnPlan {
+  int pairs = 0, reg_pairs = 0, n_units = 0, n_whole = 0, split = 1;
+  int64_t pieces() const { return (int64_t)(n_units - n_whole) * split; }
+  int grid() const { return n_whole + (int)pieces(); }
+};
+
+static double makespan(const std::vector<double>& costs, int sms) {
+  std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+  for (int i = 0; i < sms; ++i) q.push(0.0);
+  double end = 0.0;
+  for (double c : costs) {
+    double t = q.top() + c;
+    q.pop();
+    q.push(t);
+    end = std::max(end, t);
+  }
+  return end;
+}
+
+static AttnPlan plan_attention(int n_q, int n_heads, int sms) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int>, AttnPlan> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_tuple(n_q, n_heads, sms);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  AttnPlan pl;
+  pl.pairs = (n_q + 2 * AT_M - 1) / (2 * AT_M);
+  const bool ragged = (pl.pairs - 1) * 2 * AT_M + AT_M >= n_q;  // last pair has one tile
+  pl.reg_pairs = pl.pairs - (ragged ? 1 : 0);
+  pl.n_units = pl.pairs * n_heads;
+  const int n_reg = pl.reg_pairs * n_heads;
+  const double c_rag = 0.6, eps = 0.02;
+  auto cost = [&](int u) { return u < n_reg ? 1.0 : c_rag; };
+  double best = 1e300;
+  AttnPlan bp = pl;
+  bp.n_whole = pl.n_units;
+  bp.split = 1;
+  std::vector<double> costs;
+  for (int n_split = 0; n_split <= std::min(pl.n_units, 2 * sms); ++n_split) {
+    for (int split = (n_split ? 2 : 1); split <= (n_split ? 16 : 1); ++split) {
+      const int n_whole = pl.n_units - n_split;
+      costs.clear();
+      for (int u = 0; u < n_whole; ++u) costs.push_back(cost(u) + eps);
+      for (int u = n_whole; u < pl.n_units; ++u)
+        for (int s = 0; s < split; ++s) costs.push_back(cost(u) / split + eps);
+      double t = makespan(costs, sms) + (n_split ? 0.05 : 0.0);
+      if (t < best - 1e-9) {
+        best = t;
+        bp.n_whole = n_whole;
+        bp.split = split;
+      }
+    }
+  }
+  bp.pairs = pl.pairs;
+  bp.reg_pairs = pl.reg_pairs;
+  bp.n_units = pl.n_units;
+  cache[key] = bp;
+  return bp;
+}
+
+int64_t attention_workspace_bytes(int n_q, int n_heads) {
+  if (n_q <= 0 || n_heads <= 0 || num_sms() <= 0) return 0;
+  const AttnPlan pl = plan_attention(n_q, n_heads, num_sms());
+  return pl.pieces() * (2 * AT_M) * (AT_D + 2) * 4;
 }
 
 int attention_tc(const lp_attn_args* a, cudaStream_t st) {
@@ -376,6 +650,12 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
   if (rc) return rc;
   rc = make_tmap_bf16_2d(&tv, a->v_arena, (uint64_t)a->arena_rows, (uint64_t)d, (uint64_t)d, AT_N, 64);
   if (rc) return rc;
+  AttnPlan pl = plan_attention(a->n_q, a->n_heads, num_sms());
+  const int64_t need = pl.pieces() * (2 * AT_M) * (AT_D + 2) * 4;
+  if (pl.pieces() > 0 && (a->workspace == nullptr || a->workspace_bytes < need)) {
+    pl.n_whole = pl.n_units;  // no workspace: run every unit whole
+    pl.split = 1;
+  }
   AttnParams p;
   p.n_q = a->n_q;
   p.n_heads = a->n_heads;
@@ -383,11 +663,20 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
   p.out = static_cast<__nv_bfloat16*>(a->out);
   p.ldo = d;
   p.desc = a->desc;
-  dim3 grid((a->n_q + 2 * AT_M - 1) / (2 * AT_M), a->n_heads);
+  p.pairs = pl.pairs;
+  p.reg_pairs = pl.reg_pairs;
+  p.n_whole = pl.n_whole;
+  p.split = pl.split;
+  p.part_o = static_cast<float*>(a->workspace);
+  p.part_ml = p.part_o ? p.part_o + pl.pieces() * (2 * AT_M) * AT_D : nullptr;
   const int smem = AttnSmem::TOTAL;
   LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  attn_tc_kernel<<<grid, AT_THREADS, smem, st>>>(tq, tk, tv, p);
-  return launch_status("attention_tc");
+  attn_tc_kernel<<<pl.grid(), AT_THREADS, smem, st>>>(tq, tk, tv, p);
+  rc = launch_status("attention_tc");
+  if (rc || pl.n_whole == pl.n_units) return rc;
+  const int64_t warps = (int64_t)(pl.n_units - pl.n_whole) * (2 * AT_M);
+  attn_combine_kernel<<<(int)((warps * 32 + 255) / 256), 256, 0, st>>>(p);
+  return launch_status("attention_combine");
 }
 
 }  // namespace lp

@@ -163,6 +163,14 @@ class Forward:
         self.geom = L.RopeGeom(prof.head_dim, t_dim // 2, S, (dh + dw_) // 2, _p(self._sp_cos), _p(self._sp_sin))
         self.scale = float(F32(1.0) / F32(np.sqrt(prof.head_dim)))  # denoiser.py:174
         self.noise = None  # host-generated corruption noise for parity runs (device tensor)
+        # partials of the KV-split tail of the tcgen05 attention grid
+        self.attn_ws, self.attn_ws_bytes = None, 0
+        if not self.fp32:
+            nb = C.c_int64(0)
+            L.call("lp_attention_workspace", N, prof.n_heads, prof.head_dim, C.byref(nb))
+            self.attn_ws_bytes = int(nb.value)
+            if self.attn_ws_bytes:
+                self.attn_ws = torch.empty(self.attn_ws_bytes, dtype=torch.uint8, device=dev)
         self.graph = None
         self.lock = threading.Lock()
         self.probe = None  # optional callable(tag, 'begin'|'end', stream) for per-kernel timing
@@ -335,7 +343,8 @@ class Forward:
                     L.call("lp_history_noise", base, ldt, d, _p(self.noise), nl, l, kv, self.desc_ptr,
                            ar.hist_max * N, st)
             args = L.AttnArgs(ldt, N, prof.n_heads, prof.head_dim, self.scale, self.q.data_ptr(), kl, vl,
-                              self.att.data_ptr(), self.desc_ptr, ar.rows, self.max_keys())
+                              self.att.data_ptr(), self.desc_ptr, ar.rows, self.max_keys(), _p(self.attn_ws),
+                              self.attn_ws_bytes)
             if self.probe:
                 self.probe("attention", "begin", stream)
             L.call("lp_attention", C.byref(args), st)
@@ -399,7 +408,7 @@ class Forward:
             n += 2
         if prof.adaln:
             n += 4
-        per_layer = 7 + (1 if self.fp32 else 0) + (2 if self._sigma_on else 0)
+        per_layer = 7 + (1 if self.fp32 else 0) + (2 if self._sigma_on else 0) + (1 if self.attn_ws_bytes else 0)
         return n + prof.n_layers * per_layer + 3
 
     def velocity_host(self) -> np.ndarray:

@@ -22,11 +22,19 @@ def _init():
     L.init_device(0)
 
 
-def _run(fn, q, karena, varena, desc, n_heads, scale, n_kv_max):
+def _workspace(n_q, n_heads):
+    nb = C.c_int64(0)
+    L.call("lp_attention_workspace", n_q, n_heads, 128, C.byref(nb))
+    return torch.empty(max(int(nb.value), 16) // 4, dtype=torch.float32, device=DEV), int(nb.value)
+
+
+def _run(fn, q, karena, varena, desc, n_heads, scale, n_kv_max, split=True):
     out = torch.zeros_like(q)
     ddev = upload_desc(desc)
+    ws, nb = _workspace(q.shape[0], n_heads) if split else (None, 0)
     args = L.AttnArgs(L.LP_BF16, q.shape[0], n_heads, 128, scale, q.data_ptr(), karena.data_ptr(),
-                      varena.data_ptr(), out.data_ptr(), ddev.data_ptr(), karena.shape[0], n_kv_max)
+                      varena.data_ptr(), out.data_ptr(), ddev.data_ptr(), karena.shape[0], n_kv_max,
+                      ws.data_ptr() if ws is not None else None, nb)
     L.call(fn, C.byref(args), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     return out
@@ -95,3 +103,33 @@ def test_segment_order_matters_only_through_content():
     a = _run("lp_attention", q, ka, va, make_desc(3, sa, 1200, n_q, 128), heads, scale, 832)
     b = _run("lp_attention", q, kb, vb, make_desc(3, sb, 1200, n_q, 128), heads, scale, 832)
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("heads", [40, 12])
+def test_full_shape_tail_split_matches_reference(heads):
+    # 480p block: 4680 queries over [sink 1560 | 4 ring slots | current]; at
+    # 40 heads the grid tail (ragged query pairs + the last units) is split
+    # into KV pieces merged by the combine kernel; must agree with the
+    # unsplit kernel and with fp32 torch per head
+    n_q, s_tok, d = 4680, 1560, heads * 128
+    rows = s_tok + 5 * n_q
+    g = torch.Generator(device=DEV).manual_seed(heads)
+    karena = torch.randn((rows, d), generator=g, device=DEV).to(torch.bfloat16)
+    varena = torch.randn((rows, d), generator=g, device=DEV).to(torch.bfloat16)
+    q = (torch.randn((n_q, d), generator=g, device=DEV) * 2).to(torch.bfloat16)
+    order = [3, 4, 0, 1]  # ring slots oldest -> newest, wrapped
+    segs = [(0, s_tok)] + [(s_tok + n_q * s, n_q) for s in order] + [(s_tok + 2 * n_q, n_q)]
+    cur = s_tok + 2 * n_q
+    desc = make_desc(7, segs, cur, n_q, 128)
+    scale = float(np.float32(1.0) / np.float32(np.sqrt(128)))
+    n_kv = sum(n for _, n in segs)
+    ws, nb = _workspace(n_q, heads)
+    tc = _run("lp_attention", q, karena, varena, desc, heads, scale, n_kv)
+    whole = _run("lp_attention", q, karena, varena, desc, heads, scale, n_kv, split=False)
+    assert rel_l2(tc.float().cpu(), whole.float().cpu()) < 5e-3
+    for h in range(0, heads, max(1, heads // 6)):
+        ref = _ref(q[:, h * 128:(h + 1) * 128].contiguous(), karena[:, h * 128:(h + 1) * 128].contiguous(),
+                   varena[:, h * 128:(h + 1) * 128].contiguous(), segs, 1, scale)
+        assert rel_l2(tc[:, h * 128:(h + 1) * 128].float().cpu(), ref.cpu()) < 1e-2, h
+    tc2 = _run("lp_attention", q, karena, varena, desc, heads, scale, n_kv)
+    assert torch.equal(tc, tc2)
