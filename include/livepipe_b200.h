@@ -50,6 +50,8 @@ extern "C" {
 #define LP_EPI_RESID 3      /* h[r,c] = h[r,c] + gate[c] * acc   (h fp32; gate NULL => 1)  */
 #define LP_EPI_QKV 4        /* columns [0,d)->q, [d,2d)->k ring slot, [2d,3d)->v ring slot,
                                with optional per-head RMSNorm and rotary embedding         */
+#define LP_EPI_EULER 5      /* velocity head + flow step: x_out = x_in + acc * desc->dt at the
+                               latent position of (token r, patch element c)  (LP_BF16)   */
 
 #define LP_MAX_SEG 66  /* sink + up to 64 history blocks + current block */
 #define LP_MAX_PAIRS 64
@@ -126,6 +128,17 @@ typedef struct lp_qkv_epi {
   lp_rope_geom geom;
 } lp_qkv_epi;
 
+/* Velocity-head epilogue (denoiser.py:268 + flow_step latent.py:140-147):
+   token r, patch element c -> latent index of frame r / tokens_per_frame,
+   channel c / (ph*pw), pixel (gy*ph + py, gx*pw + px); ph == 0 => toy layout
+   (x[r * n + c]).  x_out = x_in + fp32(acc * dt), separately rounded.       */
+typedef struct lp_euler_epi {
+  const float* x_in;
+  float* x_out;           /* may be a peer-mapped receive slot              */
+  int32_t channels, height, width, ph, pw;
+  const lp_block_desc* desc;
+} lp_euler_epi;
+
 typedef struct lp_gemm_args {
   int32_t in_dtype;       /* LP_F32 | LP_BF16                               */
   int32_t out_dtype;      /* for STORE/RELU/GELU                            */
@@ -138,6 +151,7 @@ typedef struct lp_gemm_args {
   const float* bias;      /* [n] or NULL (STORE only)                       */
   const float* gate;      /* [n] or NULL (RESID only)                       */
   const lp_qkv_epi* qkv;  /* host pointer, LP_EPI_QKV only                  */
+  const lp_euler_epi* euler; /* host pointer, LP_EPI_EULER only             */
 } lp_gemm_args;
 LP_API int lp_gemm(const lp_gemm_args* args, void* stream);
 
@@ -195,7 +209,9 @@ LP_API int lp_norm_mod(const float* h, int rows, int d, int mode, float eps,
    (raw_layer_stride elements apart) are the un-rotated projections of the
    sink latent, computed once per sink content (RSFM: after the one-shot AAS
    swap); writes (optionally per-head-RMS-normed) rotated K and V into arena
-   rows [desc->seg_row[0], +S) of every layer (arena_layer_stride apart).   */
+   rows [desc->seg_row[0], +S) of every layer (arena_layer_stride apart).
+   v_raw == NULL: K only (the V rows do not depend on the position, so a
+   caller whose sink rows are fixed writes them once per sink content).     */
 LP_API int lp_sink_refresh(const float* k_raw, const float* v_raw, int s_tokens, int d,
                     int n_heads, int qk_norm, const float* g_k, float eps,
                     const lp_block_desc* desc, const lp_rope_geom* geom,

@@ -27,6 +27,8 @@ from .metrics import (MetricsBundle, TimelineEvent, compute_fps, compute_ttff, d
 from .model import (WAN_14B, WAN_1_3B, DenoiserWeights, DeviceWeights, LayerWeights, ModelProfile,
                     build_weights, toy_profile, wan_profile)
 from .numerics import Prng, gaussian
+from .artifacts import (export_timeline, format_timeline, frames_digest, latents_bytes, latents_digest,
+                        parse_timeline, read_latents, write_latents)
 
 # the reference's class name for the plug-in point (engine.py:200)
 ToyDenoiser = B200Denoiser

@@ -17,7 +17,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "livepipe_b200.h")
 
 LP_OK, LP_EINVAL, LP_ECUDA, LP_EUNSUPPORTED, LP_ETIMEOUT, LP_EABORT = range(6)
 LP_F32, LP_BF16 = 0, 1
-EPI_STORE, EPI_RELU, EPI_GELU, EPI_RESID, EPI_QKV = range(5)
+EPI_STORE, EPI_RELU, EPI_GELU, EPI_RESID, EPI_QKV, EPI_EULER = range(6)
 MAX_SEG = 66
 MAX_PAIRS = 64
 
@@ -48,10 +48,15 @@ class QkvEpi(C.Structure):
                 ("desc", vp), ("geom", RopeGeom)]
 
 
+class EulerEpi(C.Structure):
+    _fields_ = [("x_in", vp), ("x_out", vp), ("channels", i32), ("height", i32), ("width", i32), ("ph", i32),
+                ("pw", i32), ("desc", vp)]
+
+
 class GemmArgs(C.Structure):
     _fields_ = [("in_dtype", i32), ("out_dtype", i32), ("epilogue", i32), ("m", i32), ("n", i32),
                 ("k", i32), ("lda", i64), ("ldw", i64), ("ldc", i64), ("a", vp), ("w", vp), ("c", vp),
-                ("bias", vp), ("gate", vp), ("qkv", C.POINTER(QkvEpi))]
+                ("bias", vp), ("gate", vp), ("qkv", C.POINTER(QkvEpi)), ("euler", C.POINTER(EulerEpi))]
 
 
 class AttnArgs(C.Structure):

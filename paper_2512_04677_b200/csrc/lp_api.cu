@@ -89,12 +89,15 @@ int lp_init(int device) {
 int lp_num_sms(void) { return g_sms; }
 
 int lp_gemm(const lp_gemm_args* a, void* stream) {
-  LP_CHECK_ARG(a && a->a && a->w && (a->c || a->epilogue == LP_EPI_QKV), "lp_gemm: null argument");
+  LP_CHECK_ARG(a && a->a && a->w && (a->c || a->epilogue == LP_EPI_QKV || a->epilogue == LP_EPI_EULER),
+               "lp_gemm: null argument");
   LP_CHECK_ARG(a->m >= 0 && a->n > 0 && a->k > 0, "lp_gemm: bad shape");
   if (a->in_dtype == LP_BF16) return gemm_tc(a, S(stream));
   LP_CHECK_ARG(a->in_dtype == LP_F32, "lp_gemm: in_dtype must be LP_F32 or LP_BF16");
   if (a->epilogue == LP_EPI_QKV)
     return fail(LP_EUNSUPPORTED, "lp_gemm: fp32 QKV epilogue is lp_gemm(STORE) + lp_qkv_post");
+  if (a->epilogue == LP_EPI_EULER)
+    return fail(LP_EUNSUPPORTED, "lp_gemm: fp32 EULER epilogue is lp_gemm(STORE) + lp_unpatchify_euler");
   return gemm_f32(a, S(stream));
 }
 
@@ -144,7 +147,7 @@ int lp_sink_refresh(const float* k_raw, const float* v_raw, int s_tokens, int d,
                     const float* g_k, float eps, const lp_block_desc* desc, const lp_rope_geom* geom,
                     void* k_arena, void* v_arena, int arena_dtype, int n_layers, int64_t raw_layer_stride,
                     int64_t arena_layer_stride, void* stream) {
-  LP_CHECK_ARG(k_raw && v_raw && desc && geom && k_arena && v_arena, "lp_sink_refresh: null argument");
+  LP_CHECK_ARG(k_raw && desc && geom && k_arena && v_arena, "lp_sink_refresh: null argument");
   return sink_refresh(k_raw, v_raw, s_tokens, d, n_heads, qk_norm, g_k, eps, desc, *geom, k_arena, v_arena,
                       arena_dtype, n_layers, raw_layer_stride, arena_layer_stride, S(stream));
 }

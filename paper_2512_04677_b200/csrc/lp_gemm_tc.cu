@@ -31,6 +31,7 @@ struct GemmParams {
   const float* bias;
   const float* gate;
   lp_qkv_epi qkv;
+  lp_euler_epi euler;
 };
 
 template <int BN>
@@ -228,6 +229,34 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
           if (!valid) continue;
+          if (p.epilogue == LP_EPI_EULER) {
+            const lp_euler_epi& e = p.euler;
+            const float dt = e.desc->dt;
+            int64_t base;
+            int gy = 0, gx = 0;
+            if (e.ph == 0) {
+              base = (int64_t)row * p.n;
+            } else {
+              const int hp = e.height / e.ph, wp = e.width / e.pw, tpf = hp * wp;
+              const int f = row / tpf, tok = row % tpf;
+              gy = tok / wp;
+              gx = tok % wp;
+              base = (int64_t)f * e.channels * e.height * e.width;
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int c = col + j;
+              int64_t idx;
+              if (e.ph == 0) {
+                idx = base + c;
+              } else {
+                const int pp = e.ph * e.pw, ch = c / pp, py = (c % pp) / e.pw, px = c % e.pw;
+                idx = base + ((int64_t)ch * e.height + gy * e.ph + py) * e.width + gx * e.pw + px;
+              }
+              e.x_out[idx] = __fadd_rn(e.x_in[idx], __fmul_rn(v[j], dt));
+            }
+            continue;
+          }
           if (p.epilogue == LP_EPI_RESID) {
             // all loads first (h and gate may alias as far as the compiler
             // knows; interleaving loads with stores serialises DRAM round trips)
@@ -321,6 +350,13 @@ int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
   p.bias = a->bias;
   p.gate = a->gate;
   memset(&p.qkv, 0, sizeof(p.qkv));
+  memset(&p.euler, 0, sizeof(p.euler));
+  if (a->epilogue == LP_EPI_EULER) {
+    LP_CHECK_ARG(a->euler != nullptr && a->euler->x_in && a->euler->x_out && a->euler->desc,
+                 "gemm_tc: EULER epilogue needs euler args");
+    p.euler = *a->euler;
+    LP_CHECK_ARG(p.euler.ph == 0 || a->n == p.euler.channels * p.euler.ph * p.euler.pw, "gemm_tc: EULER shape");
+  }
   if (a->epilogue == LP_EPI_QKV) {
     LP_CHECK_ARG(a->qkv != nullptr, "gemm_tc: QKV epilogue needs qkv args");
     p.qkv = *a->qkv;

@@ -52,8 +52,24 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return red[0];
 }
 
-// One CTA per row, float4 loads, two-pass mean/variance in fp32.
-template <typename OutT, int THREADS>
+// One CTA per row, float4 loads, two-pass mean/variance in fp32.  The row
+// is read from HBM once: up to NV float4 per thread stay in registers
+// (d <= THREADS*4*NV, the 14B/1.3B widths), wider rows re-read through L1/L2.
+template <typename OutT>
+__device__ __forceinline__ void store4(OutT* o, const float* y) {
+  if constexpr (sizeof(OutT) == 2) {
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(y[0], y[1]);
+    __nv_bfloat162 p1 = __floats2bfloat162_rn(y[2], y[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&p0);
+    u.y = *reinterpret_cast<uint32_t*>(&p1);
+    *reinterpret_cast<uint2*>(o) = u;
+  } else {
+    *reinterpret_cast<float4*>(o) = make_float4(y[0], y[1], y[2], y[3]);
+  }
+}
+
+template <typename OutT, int THREADS, int NV = 8>
 __global__ void __launch_bounds__(THREADS) norm_mod_kernel(const float* __restrict__ h, int d, int mode,
                                                            float eps, const float* __restrict__ shift,
                                                            const float* __restrict__ scale,
@@ -66,36 +82,61 @@ __global__ void __launch_bounds__(THREADS) norm_mod_kernel(const float* __restri
     for (int c = threadIdx.x; c < d; c += THREADS) o[c] = from_f32<OutT>(x[c]);
     return;
   }
+  const bool cached = d <= THREADS * 4 * NV;
+  float4 v[NV];
   float s = 0.0f;
-  for (int c = threadIdx.x * 4; c < d; c += THREADS * 4) {
-    float4 v = *reinterpret_cast<const float4*>(x + c);
-    s += (v.x + v.y) + (v.z + v.w);
+  if (cached) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * THREADS + threadIdx.x) * 4;
+      v[i] = c < d ? *reinterpret_cast<const float4*>(x + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    }
+  } else {
+    for (int c = threadIdx.x * 4; c < d; c += THREADS * 4) {
+      float4 t = *reinterpret_cast<const float4*>(x + c);
+      s += (t.x + t.y) + (t.z + t.w);
+    }
   }
   const float mu = block_sum<THREADS>(s, red) / d;
   float q = 0.0f;
-  for (int c = threadIdx.x * 4; c < d; c += THREADS * 4) {
-    float4 v = *reinterpret_cast<const float4*>(x + c);
-    float a = v.x - mu, b = v.y - mu, e = v.z - mu, f = v.w - mu;
-    q += (a * a + b * b) + (e * e + f * f);
+  if (cached) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * THREADS + threadIdx.x) * 4;
+      if (c < d) {
+        float a = v[i].x - mu, b = v[i].y - mu, e = v[i].z - mu, f = v[i].w - mu;
+        q += (a * a + b * b) + (e * e + f * f);
+      }
+    }
+  } else {
+    for (int c = threadIdx.x * 4; c < d; c += THREADS * 4) {
+      float4 t = *reinterpret_cast<const float4*>(x + c);
+      float a = t.x - mu, b = t.y - mu, e = t.z - mu, f = t.w - mu;
+      q += (a * a + b * b) + (e * e + f * f);
+    }
   }
   const float rstd = rsqrtf(block_sum<THREADS>(q, red) / d + eps);
-  for (int c = threadIdx.x * 4; c < d; c += THREADS * 4) {
-    float4 v = *reinterpret_cast<const float4*>(x + c);
-    float y[4] = {(v.x - mu) * rstd, (v.y - mu) * rstd, (v.z - mu) * rstd, (v.w - mu) * rstd};
+  auto emit = [&](int c, float4 t) {
+    float y[4] = {(t.x - mu) * rstd, (t.y - mu) * rstd, (t.z - mu) * rstd, (t.w - mu) * rstd};
     if (mode == 2) {
+      const float4 sc = __ldg(reinterpret_cast<const float4*>(scale + c));
+      const float4 sh = __ldg(reinterpret_cast<const float4*>(shift + c));
+      y[0] = y[0] * (1.0f + sc.x) + sh.x;
+      y[1] = y[1] * (1.0f + sc.y) + sh.y;
+      y[2] = y[2] * (1.0f + sc.z) + sh.z;
+      y[3] = y[3] * (1.0f + sc.w) + sh.w;
+    }
+    store4<OutT>(o + c, y);
+  };
+  if (cached) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) y[j] = y[j] * (1.0f + scale[c + j]) + shift[c + j];
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * THREADS + threadIdx.x) * 4;
+      if (c < d) emit(c, v[i]);
     }
-    if constexpr (sizeof(OutT) == 2) {
-      __nv_bfloat162 p0 = __floats2bfloat162_rn(y[0], y[1]);
-      __nv_bfloat162 p1 = __floats2bfloat162_rn(y[2], y[3]);
-      uint2 u;
-      u.x = *reinterpret_cast<uint32_t*>(&p0);
-      u.y = *reinterpret_cast<uint32_t*>(&p1);
-      *reinterpret_cast<uint2*>(o + c) = u;
-    } else {
-      *reinterpret_cast<float4*>(o + c) = make_float4(y[0], y[1], y[2], y[3]);
-    }
+  } else {
+    for (int c = threadIdx.x * 4; c < d; c += THREADS * 4) emit(c, *reinterpret_cast<const float4*>(x + c));
   }
 }
 
@@ -113,9 +154,7 @@ __global__ void sink_refresh_kernel(const float* __restrict__ kraw, const float*
   if (tok >= s_tok) return;
   const int layer = blockIdx.y;
   kraw += layer * raw_stride;
-  vraw += layer * raw_stride;
   karena += layer * arena_stride;
-  varena += layer * arena_stride;
   if (g_k) g_k += (int64_t)layer * d;
   const int hd = geom.head_dim;
   const int row = desc->seg_row[0] + tok;
@@ -123,7 +162,10 @@ __global__ void sink_refresh_kernel(const float* __restrict__ kraw, const float*
   float inv = 1.0f;
   if (qk_norm) {
     float ss = 0.0f;
-    for (int c = lane; c < hd; c += 32) ss += k[c] * k[c];
+    for (int c = lane * 2; c < hd; c += 64) {
+      const float2 t = *reinterpret_cast<const float2*>(k + c);
+      ss += t.x * t.x + t.y * t.y;
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     inv = rsqrtf(ss / hd + eps);
@@ -131,7 +173,8 @@ __global__ void sink_refresh_kernel(const float* __restrict__ kraw, const float*
   RopeTab rt{desc->sink_cos, desc->sink_sin, geom};
   T* ko = karena + (int64_t)row * d + head * hd;
   for (int p = lane; p < hd / 2; p += 32) {
-    float x = k[2 * p], y = k[2 * p + 1];
+    const float2 t = *reinterpret_cast<const float2*>(k + 2 * p);
+    float x = t.x, y = t.y;
     if (qk_norm) {
       x = x * inv * (g_k ? g_k[head * hd + 2 * p] : 1.0f);
       y = y * inv * (g_k ? g_k[head * hd + 2 * p + 1] : 1.0f);
@@ -142,6 +185,9 @@ __global__ void sink_refresh_kernel(const float* __restrict__ kraw, const float*
     ko[2 * p] = from_f32<T>(xo);
     ko[2 * p + 1] = from_f32<T>(yo);
   }
+  if (vraw == nullptr) return;  // V rows are position-independent: written once per sink content
+  vraw += layer * raw_stride;
+  varena += layer * arena_stride;
   const float* v = vraw + (int64_t)tok * d + head * hd;
   T* vo = varena + (int64_t)row * d + head * hd;
   for (int c = lane; c < hd; c += 32) vo[c] = from_f32<T>(v[c]);

@@ -245,6 +245,7 @@ class B200Denoiser:
             ws = self._ws.get(t_index)
             if ws is None:
                 fw = Forward(self.dw, n_frames, self._pool.arena)
+                fw.fuse_euler = False  # denoise_block returns the velocity itself
                 stream = torch.cuda.Stream(self.device)
                 ws = self._ws[t_index] = (fw, stream, min(t_index, self._pool.n_workspaces - 1))
             return ws

@@ -33,7 +33,7 @@ import torch
 
 from . import _lib as L
 from .denoiser import B200Denoiser, BlockCond
-from .kvcache import RollingKvCache, SinkSlot, aas_update, corrupt_history, corruption_prng, receive_sink, \
+from .kvcache import RingIndex, RollingKvCache, SinkSlot, aas_update, corrupt_history, corruption_prng, receive_sink, \
     rolling_rope_index
 from .latent import Conditions, LatentBlock, TimestepSchedule, ToyVideoCodec, flow_step, synthetic_conditions
 from .metrics import MetricsBundle, TimelineEvent, drift_metric, metrics_from_timeline
@@ -214,8 +214,9 @@ class Stage:
             self.arena = KvArena(prof, n_tok, self.L + 1, self.L if self.sigma_on else 0, dw.dtype,
                                  f"cuda:{device}")
             self.fw = Forward(dw, cfg.frames_per_block, self.arena)
+            self.fw.sink_v_static = True  # sink rows fixed at [0, S) (write_inputs sink_row=0)
         self.fw.set_history_noise(self.sigma_on, None)
-        self.ring: list = []  # block indices, oldest first (RollingKvCache replay, kvcache.py:41-56)
+        self.ring = RingIndex(self.L)  # RollingKvCache replay on ring slots (kvcache.py:41-56)
         self.graph = None
         self.nfe = 0
         self.ev = []  # (block, start event, end event)
@@ -225,7 +226,7 @@ class Stage:
             self.fw.set_sink(torch.from_numpy(np.asarray(sink, F32).copy()), stream=self.stream)
 
     def visible(self) -> list:
-        return list(self.ring)
+        return list(self.ring.blocks)
 
     def prepare(self, i: int) -> None:
         """Stage the descriptor for block i (cache view = current ring)."""
@@ -233,22 +234,22 @@ class Stage:
         segs = []
         noise = None
         sigma = _sigma(self.cfg, self.rt, self.j) if self.sigma_on else 0.0
-        for e, b in enumerate(self.ring):
-            row = ar.slot_row(b % (self.L + 1))
+        for e, (b, slot) in enumerate(self.ring.view()):
+            row = ar.slot_row(slot)
             segs.append((ar.scratch_row(e) if self.sigma_on else row, ar.n_tokens, row))
-        if self.sigma_on and not cfg.device_inputs and self.ring:
+        if self.sigma_on and not cfg.device_inputs and len(self.ring):
             # reference draw order (kvcache.py:121-137): per entry keys of all layers, then values
             g = corruption_prng(cfg.noise_seed, i, self.j)
             prof = cfg.model_profile
             shape = (ar.n_tokens, prof.model_dim)
             arr = np.stack([np.stack([np.stack([g.normal(shape) for _ in range(prof.n_layers)])
-                                      for _kv in range(2)]) for _ in self.ring])
+                                      for _kv in range(2)]) for _ in self.ring.blocks])
             noise = torch.from_numpy(arr).to(f"cuda:{self.device}")
         if self.sigma_on:
             self._noise_keep = noise
             fw.noise = noise
         key = (cfg.noise_seed * 0x9E3779B97F4A7C15 + i * 4096 + self.j) & ((1 << 64) - 1)
-        fw.write_inputs(i, self.j, cfg.steps, segs, ar.slot_row(i % (self.L + 1)),
+        fw.write_inputs(i, self.j, cfg.steps, segs, ar.slot_row(self.ring.write_slot(i)),
                         rolling_rope_index(i, cfg.sink_delta), self.rt.schedule.dt,
                         self.rt.conditions.audio_for(i), self.rt.conditions.prompt, sigma=sigma, noise_key=key,
                         stream=self.stream)
@@ -292,9 +293,7 @@ class Stage:
                 e1.record(self.stream)
                 self.ev.append((i, e0, e1))
         self.nfe += 1
-        self.ring.append(i)
-        if len(self.ring) > self.L:
-            self.ring.pop(0)
+        self.ring.push(i)
 
 
 def _events_to_timeline(stages, t0_event, decode_times, k_of_j):

@@ -280,6 +280,11 @@ class Forward:
             self._proj(st, xs.data_ptr(), S, d, w, d, self.v_raw[l].data_ptr(), d, L.EPI_STORE, L.LP_F32,
                        w_col0=2 * d)
         self._sink_tmp = (sh, xs)
+        if self.sink_v_static:
+            # V rows of the sink do not depend on the position: write them once
+            # per sink content (arena rows [0, S)); the per-block refresh is K only
+            with torch.cuda.stream(s_obj):
+                self.arena.v[:, :S].copy_(self.v_raw)
 
     # ---------------------------------------------------------- forward ------
     def launch(self, stream=None, x_out: torch.Tensor | None = None) -> None:
@@ -311,7 +316,8 @@ class Forward:
         else:
             L.call("lp_add_row", self.x_in.data_ptr(), self.c.data_ptr(), self.h.data_ptr(), N, d, st)
         # sink K/V at i + delta for every layer (kvcache.py:86-90)
-        L.call("lp_sink_refresh", self.k_raw.data_ptr(), self.v_raw.data_ptr(), prof.tokens_per_frame, d,
+        L.call("lp_sink_refresh", self.k_raw.data_ptr(), None if self.sink_v_static else self.v_raw.data_ptr(),
+               prof.tokens_per_frame, d,
                prof.n_heads, int(prof.qk_norm), _p(dw.g_k), prof.eps, self.desc_ptr, C.byref(self.geom),
                ar.k.data_ptr(), ar.v.data_ptr(), ldt, nl, prof.tokens_per_frame * d, ar.layer_stride, st)
         esz = ar.k.element_size()
@@ -377,16 +383,36 @@ class Forward:
         else:
             L.call("lp_norm_mod", self.h.data_ptr(), N, d, 1 if prof.pre_ln else 0, prof.eps, None, None,
                    self.xa.data_ptr(), ldt, st)
-        self._proj(st, self.xa.data_ptr(), N, d, dw.w_vel, prof.out_dim, self.vel.data_ptr(), prof.out_dim,
-                   L.EPI_STORE, L.LP_F32)
-        if prof.patched:
-            L.call("lp_unpatchify_euler", self.x_in.data_ptr(), self.vel.data_ptr(), self.n_frames, prof.channels,
-                   prof.height, prof.width, prof.patch[0], prof.patch[1], self.desc_ptr, xo.data_ptr(), st)
+        if self.fp32 or not self.fuse_euler:
+            self._proj(st, self.xa.data_ptr(), N, d, dw.w_vel, prof.out_dim, self.vel.data_ptr(), prof.out_dim,
+                       L.EPI_STORE, L.LP_F32)
+            if prof.patched:
+                L.call("lp_unpatchify_euler", self.x_in.data_ptr(), self.vel.data_ptr(), self.n_frames,
+                       prof.channels, prof.height, prof.width, prof.patch[0], prof.patch[1], self.desc_ptr,
+                       xo.data_ptr(), st)
+            else:
+                L.call("lp_unpatchify_euler", self.x_in.data_ptr(), self.vel.data_ptr(), 1, 1, 1, N * d, 0, 0,
+                       self.desc_ptr, xo.data_ptr(), st)
         else:
-            L.call("lp_unpatchify_euler", self.x_in.data_ptr(), self.vel.data_ptr(), 1, 1, 1, N * d, 0, 0,
-                   self.desc_ptr, xo.data_ptr(), st)
+            # velocity head with the flow step fused into the GEMM epilogue (K6)
+            ph, pw = prof.patch if prof.patched else (0, 0)
+            self._euler = L.EulerEpi(self.x_in.data_ptr(), xo.data_ptr(), prof.channels, prof.height, prof.width,
+                                     ph, pw, self.desc_ptr)
+            args = L.GemmArgs()
+            args.in_dtype, args.out_dtype, args.epilogue = self.dw.ldt, L.LP_F32, L.EPI_EULER
+            args.m, args.n, args.k = N, prof.out_dim, d
+            args.lda, args.ldw, args.ldc = d, d, prof.out_dim
+            args.a, args.w, args.c = self.xa.data_ptr(), dw.w_vel.data_ptr(), 0
+            args.euler = C.pointer(self._euler)
+            L.call("lp_gemm", C.byref(args), st)
 
     _sigma_on = False
+    # bf16: fuse the flow step into the velocity-head GEMM epilogue (engine
+    # stages); the drop-in denoiser needs the raw velocity and turns it off
+    fuse_euler = True
+    # engine stages keep the sink at arena rows [0, S) (sink_row 0): sink V is
+    # written by set_sink, not re-written every block
+    sink_v_static = False
 
     def max_keys(self) -> int:
         """Upper bound of visible keys: sink + every ring slot (or the
@@ -409,7 +435,7 @@ class Forward:
         if prof.adaln:
             n += 4
         per_layer = 7 + (1 if self.fp32 else 0) + (2 if self._sigma_on else 0) + (1 if self.attn_ws_bytes else 0)
-        return n + prof.n_layers * per_layer + 3
+        return n + prof.n_layers * per_layer + (3 if (self.fp32 or not self.fuse_euler) else 2)
 
     def velocity_host(self) -> np.ndarray:
         """(F, latent_dim) velocity of the last forward (host copy)."""

@@ -141,3 +141,39 @@ def test_f32_pinned_gemm_is_bitwise_reference_order():
     c = torch.zeros((37, 45), device=DEV)
     _gemm(ta, tb, c, L.EPI_STORE, L.LP_F32, in_dtype=L.LP_F32)
     assert c.cpu().numpy().tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("patched", [True, False])
+def test_euler_epilogue(patched):
+    # velocity head + flow step fused (K6): x_out = x_in + unpatchify(a . W^T) * dt
+    frames, C_, H, W, ph, pw = 3, 16, 8, 12, 2, 2
+    if patched:
+        tpf, pd = (H // ph) * (W // pw), C_ * ph * pw
+        m, n = frames * tpf, pd
+    else:
+        m, n = 96, 128
+    k = 256
+    a, w = _ab(m, k, n, 5)
+    v = a.float() @ w.float().T
+    dt = -0.25
+    desc = upload_desc(make_desc(3, [(0, 1), (0, m)], 0, m, 128, dt=dt))
+    lat = C_ * H * W
+    if patched:
+        x_in = torch.randn((frames, lat), device=DEV)
+        vu = v.reshape(frames, H // ph, W // pw, C_, ph, pw).permute(0, 3, 1, 4, 2, 5).reshape(frames, lat)
+    else:
+        x_in = torch.randn((m, n), device=DEV)
+        vu = v
+    x_out = torch.zeros_like(x_in)
+    ep = L.EulerEpi(x_in.data_ptr(), x_out.data_ptr(), C_ if patched else 0, H, W, ph if patched else 0,
+                    pw if patched else 0, desc.data_ptr())
+    args = L.GemmArgs()
+    args.in_dtype, args.out_dtype, args.epilogue = L.LP_BF16, L.LP_F32, L.EPI_EULER
+    args.m, args.n, args.k = m, n, k
+    args.lda, args.ldw, args.ldc = k, k, n
+    args.a, args.w, args.c = a.data_ptr(), w.data_ptr(), None
+    args.euler = C.pointer(ep)
+    L.call("lp_gemm", C.byref(args), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref = x_in + vu * dt
+    assert rel_l2(x_out.cpu(), ref.cpu()) < 1e-5

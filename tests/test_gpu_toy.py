@@ -173,3 +173,19 @@ def test_oracle_restatement_on_device_inputs():
     res = lp.run_sequential(lp.EngineConfig(mode="sequential", steps=3, blocks=5, cache_capacity=2,
                                             history_sigma=0.1))
     assert rel_l2(np.stack([b.values for b in res.blocks]), np.stack(ob)) < TOL_FP32
+
+
+def test_measured_timeline_export(tmp_path):
+    # CUDA-event intervals -> TimelineEvent -> the
+    # reference's metrics and timeline file format
+    res = lp.run_tpp(lp.EngineConfig(mode="tpp", steps=4, blocks=4))
+    assert res.timeline and res.metrics is not None
+    kinds = {e.kind for e in res.timeline}
+    assert kinds == {"denoise", "decode"}
+    assert sorted({e.stage for e in res.timeline}) == [1, 2, 3, 4, 5]
+    assert res.metrics.fps > 0 and res.metrics.nfe == 16
+    p = lp.export_timeline(res.timeline, str(tmp_path / "tl.csv"), res.metrics)
+    ev, rec = lp.parse_timeline(p)
+    assert tuple(ev) == res.timeline and rec["nfe"] == 16
+    q = lp.write_latents(str(tmp_path / "x.lpd"), res.blocks)
+    np.testing.assert_array_equal(lp.read_latents(q), np.stack([b.values for b in res.blocks]))
