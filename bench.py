@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N>1 (gloo lets several ranks share one GPU in tests)")
     return ap.parse_args()
 
 
@@ -321,8 +323,13 @@ def run_dist(args, rank, world, local):
     import paper_2512_04677_b200 as lp
     from paper_2512_04677_b200 import tpp_dist
 
+    ndev = torch.cuda.device_count()
+    local = local % ndev  # ranks may share a GPU (functional checks on a 1-GPU box)
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if args.dist_backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        dist.init_process_group("gloo")
     prof = profile_for(args.config)
     T, Lc = 4, 4
     cfg = lp.EngineConfig(mode="tpp", steps=T, cache_capacity=Lc, frames_per_block=3, profile=prof,
@@ -359,7 +366,8 @@ def run_dist(args, rank, world, local):
         run.finish()
         dist.barrier()
     el = e0.elapsed_time(ends[-1]) / 1e3
-    t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{local}")
+    dd = f"cuda:{local}" if args.dist_backend == "nccl" else "cpu"
+    t = torch.tensor([el], dtype=torch.float64, device=dd)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     job_s = float(t.item())
     fps = FRAMES_PER_BLOCK_VIDEO * K * role.n_pipes / job_s
@@ -381,7 +389,7 @@ def run_dist(args, rank, world, local):
     e3.record(s)
     torch.cuda.synchronize(local)
     run.finish()
-    t = torch.tensor([e2.elapsed_time(e3) / 1e3], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([e2.elapsed_time(e3) / 1e3], dtype=torch.float64, device=dd)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_fps = FRAMES_PER_BLOCK_VIDEO * K * role.n_pipes / float(t.item())
 
@@ -390,10 +398,10 @@ def run_dist(args, rank, world, local):
         kern, _ = probe_kernels(be.stages, lambda: run.step(base + K, noise=noise_dev[W + K], out=out_dev), s)
         run.finish()
     roof = roofline(prof, kern, n_tok, n_kv_steady)
-    steady_t = torch.tensor([steady or 0.0], dtype=torch.float64, device=f"cuda:{local}")
+    steady_t = torch.tensor([steady or 0.0], dtype=torch.float64, device=dd)
     dist.all_reduce(steady_t, op=dist.ReduceOp.MAX)
     launches = torch.tensor([sum(st.fw.kernels_per_forward() for st in be.stages) * K], dtype=torch.int64,
-                            device=f"cuda:{local}")
+                            device=dd)
     dist.all_reduce(launches)
     peaks, _ = _peaks()
     peak_tf = peaks.get("bf16_tflops", 1590.0)

@@ -12,7 +12,7 @@ import re
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblivepipe_b200.so")
+LIB_PATH = os.environ.get("LIVEPIPE_LIB") or os.path.join(HERE, "liblivepipe_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "livepipe_b200.h")
 
 LP_OK, LP_EINVAL, LP_ECUDA, LP_EUNSUPPORTED, LP_ETIMEOUT, LP_EABORT = range(6)

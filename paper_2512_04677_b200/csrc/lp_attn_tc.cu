@@ -46,24 +46,24 @@ namespace lp {
 
 using namespace sm100;
 
-constexpr int AT_M = 128;      // query rows per softmax warpgroup (one Q tile)
-constexpr int AT_N = 64;       // keys per KV tile
+constexpr int AT_M = 128;      // query rows per softmax warpgroup
+constexpr int AT_N = 128;      // keys per tile
 constexpr int AT_D = 128;      // head dim
-constexpr int AT_THREADS = 320;
-constexpr int AT_KST = 4;                              // K and V smem ring stages
-constexpr int AT_Q_BYTES = AT_M * AT_D * 2;            // 32 KB per Q tile
-constexpr int AT_QHALF = AT_Q_BYTES / 2;               // one 64-column SW128 block of Q
-constexpr int AT_KV_BYTES = AT_N * AT_D * 2;           // 16 KB per K or V tile
-constexpr int AT_KVHALF = AT_KV_BYTES / 2;             // one 64-column SW128 block of K / V
-constexpr float AT_RESCALE_THRESH = 8.0f;              // log2 units: rescale O when the max grows > 2^8
+constexpr int AT_THREADS = 384;  // WG0: TMA warp, MMA warp, 2 idle; WG1, WG2: softmax of Q tiles A, B
+constexpr int AT_REG_CTRL = 56;  // setmaxnreg budget of the control warpgroup
+constexpr int AT_REG_SOFTMAX = 224;  // ... and of each softmax warpgroup (56*128 + 224*256 <= 64K)
+constexpr int AT_TILE_BYTES = AT_N * AT_D * 2;  // 32 KB
+constexpr int AT_HALF = AT_TILE_BYTES / 2;      // one 64-column SW128 block
+constexpr float AT_RESCALE_THRESH = 8.0f;       // log2 units: rescale O when the max grows > 2^8
 
 struct AttnSmem {
-  static constexpr int Q_OFF = 0;                               // Q_A, Q_B
-  static constexpr int K_OFF = Q_OFF + 2 * AT_Q_BYTES;          // AT_KST stages
-  static constexpr int V_OFF = K_OFF + AT_KST * AT_KV_BYTES;    // AT_KST stages
-  static constexpr int BAR_OFF = V_OFF + AT_KST * AT_KV_BYTES;
-  static constexpr int SEG_OFF = BAR_OFF + 512;
+  static constexpr int Q_OFF = 0;                           // Q_A, Q_B
+  static constexpr int K_OFF = Q_OFF + 2 * AT_TILE_BYTES;   // 2 stages
+  static constexpr int V_OFF = K_OFF + 2 * AT_TILE_BYTES;   // 2 stages
+  static constexpr int BAR_OFF = V_OFF + 2 * AT_TILE_BYTES;
+  static constexpr int SEG_OFF = BAR_OFF + 256;
   static constexpr int TOTAL = SEG_OFF + 2 * LP_MAX_SEG * 4 + 16 + 1024;
+  static_assert(2 * LP_MAX_SEG * 4 + 16 >= 2 * LP_MAX_SEG * 4 + 3 * 4, "segment scratch");
 };
 
 struct AttnParams {
@@ -201,15 +201,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AttnSmem::BAR_OFF);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;                // [AT_KST]
-  uint64_t* k_empty = k_full + AT_KST;        // [AT_KST]
-  uint64_t* v_full = k_empty + AT_KST;        // [AT_KST]
-  uint64_t* v_empty = v_full + AT_KST;        // [AT_KST]
-  uint64_t* s_full = v_empty + AT_KST;        // [Q tile][S buffer]
-  uint64_t* p_full = s_full + 4;              // [Q tile]
-  uint64_t* o_ready = p_full + 2;             // [Q tile]: P.V of one KV tile complete
-  uint64_t* o_done = o_ready + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* k_empty = bars + 3;  // [2]
+  uint64_t* v_full = bars + 5;   // [2]
+  uint64_t* v_empty = bars + 7;  // [2]
+  uint64_t* s_full = bars + 9;   // [2] per Q tile
+  uint64_t* p_full = bars + 11;  // [2] per Q tile
+  uint64_t* o_done = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
   int* seg_row = reinterpret_cast<int*>(smem + AttnSmem::SEG_OFF);
   int* seg_len = seg_row + LP_MAX_SEG;
   int* n_seg_s = seg_len + LP_MAX_SEG;
@@ -248,16 +247,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
-    for (int i = 0; i < AT_KST; ++i) {
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
-    }
-    for (int i = 0; i < 4; ++i) mbar_init(&s_full[i], 1);
-    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
-      mbar_init(&o_ready[i], 1);
     }
     mbar_init(o_done, 1);
     fence_barrier_init();
@@ -270,17 +266,16 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   const int n_tiles = n_seg_s[1];
   const int t_first = n_seg_s[2];
   const int col0 = head * AT_D;
-  // TMEM columns: S_x buffer b at x*128 + b*64 (P_x aliases its first 32
-  // columns as packed bf16), O_x at 256 + x*128.
 
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(AT_REG_CTRL));
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     if (elect_one()) {
       uint8_t* sq = smem + AttnSmem::Q_OFF;
-      mbar_arrive_expect_tx(q_full, (two ? 2 : 1) * AT_Q_BYTES);
+      mbar_arrive_expect_tx(q_full, (two ? 2 : 1) * AT_TILE_BYTES);
       for (int t = 0; t < (two ? 2 : 1); ++t) {
-        tma_load_2d(sq + t * AT_Q_BYTES, &tmQ, q_full, col0, q0 + t * AT_M);
-        tma_load_2d(sq + t * AT_Q_BYTES + AT_QHALF, &tmQ, q_full, col0 + 64, q0 + t * AT_M);
+        tma_load_2d(sq + t * AT_TILE_BYTES, &tmQ, q_full, col0, q0 + t * AT_M);
+        tma_load_2d(sq + t * AT_TILE_BYTES + AT_HALF, &tmQ, q_full, col0 + 64, q0 + t * AT_M);
       }
       TileCursor ck, cv;
       ck.init(seg_row, seg_len, n_seg_s[0]);
@@ -290,101 +285,93 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       const uint64_t pol = l2_policy_evict_last();
       for (int t = 0; t <= n_tiles; ++t) {
         if (t < n_tiles) {
-          const int b = t % AT_KST;
-          mbar_wait(&k_empty[b], ((t / AT_KST) & 1) ^ 1);
-          uint8_t* sk = smem + AttnSmem::K_OFF + b * AT_KV_BYTES;
-          mbar_arrive_expect_tx(&k_full[b], AT_KV_BYTES);
+          const int b = t & 1;
+          mbar_wait(&k_empty[b], ((t >> 1) & 1) ^ 1);
+          uint8_t* sk = smem + AttnSmem::K_OFF + b * AT_TILE_BYTES;
+          mbar_arrive_expect_tx(&k_full[b], AT_TILE_BYTES);
           tma_load_2d_hint(sk, &tmK, &k_full[b], col0, ck.cur_row(), pol);
-          tma_load_2d_hint(sk + AT_KVHALF, &tmK, &k_full[b], col0 + 64, ck.cur_row(), pol);
+          tma_load_2d_hint(sk + AT_HALF, &tmK, &k_full[b], col0 + 64, ck.cur_row(), pol);
           ck.next();
         }
         if (t >= 1) {
-          const int u = t - 1, b = u % AT_KST;
-          mbar_wait(&v_empty[b], ((u / AT_KST) & 1) ^ 1);
-          uint8_t* sv = smem + AttnSmem::V_OFF + b * AT_KV_BYTES;
-          mbar_arrive_expect_tx(&v_full[b], AT_KV_BYTES);
+          const int u = t - 1, b = u & 1;
+          mbar_wait(&v_empty[b], ((u >> 1) & 1) ^ 1);
+          uint8_t* sv = smem + AttnSmem::V_OFF + b * AT_TILE_BYTES;
+          mbar_arrive_expect_tx(&v_full[b], AT_TILE_BYTES);
           tma_load_2d_hint(sv, &tmV, &v_full[b], col0, cv.cur_row(), pol);
-          tma_load_2d_hint(sv + AT_KVHALF, &tmV, &v_full[b], col0 + 64, cv.cur_row(), pol);
+          tma_load_2d_hint(sv + AT_HALF, &tmV, &v_full[b], col0 + 64, cv.cur_row(), pol);
           cv.next();
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    // Per Q tile x the S buffer of KV tile t is t & 1: S_x(t+2) is issued
-    // right after P_x(t).V (same buffer; one thread's tcgen05.mma stream
-    // executes in order), so S_x(t+1) is already computed while the softmax
-    // warpgroup works on tile t.
     constexpr uint32_t IDESC_S = idesc_bf16_f32(AT_M, AT_N);               // Q K^T: both K-major
     constexpr uint32_t IDESC_O = idesc_bf16_f32(AT_M, AT_D, false, true);  // P V: P in TMEM, V MN-major
     const uint32_t sq = smem_u32(smem + AttnSmem::Q_OFF);
-    auto issue_s = [&](int t, int x) {  // S_x(t) = Q_x K_t^T into buffer t & 1
-      const uint32_t sk = smem_u32(smem + AttnSmem::K_OFF + (t % AT_KST) * AT_KV_BYTES);
-      const uint32_t sqx = sq + x * AT_Q_BYTES;
-      const uint32_t ts = tmem_base + x * 128 + (t & 1) * AT_N;
+    auto issue_s = [&](int t, int x) {  // S_x(t) = Q_x K_t^T
+      const uint32_t sk = smem_u32(smem + AttnSmem::K_OFF + (t & 1) * AT_TILE_BYTES);
+      const uint32_t sqx = sq + x * AT_TILE_BYTES;
 #pragma unroll
       for (int kk = 0; kk < AT_D / 16; ++kk) {
-        const uint32_t oq = (kk >> 2) * AT_QHALF + (kk & 3) * 32;
-        const uint32_t ok = (kk >> 2) * AT_KVHALF + (kk & 3) * 32;
-        mma_bf16_ss(ts, sdesc_kmajor_sw128(sqx + oq), sdesc_kmajor_sw128(sk + ok), IDESC_S, kk != 0);
+        const uint32_t off = (kk >> 2) * AT_HALF + (kk & 3) * 32;
+        mma_bf16_ss(tmem_base + x * AT_N, sdesc_kmajor_sw128(sqx + off), sdesc_kmajor_sw128(sk + off), IDESC_S,
+                    kk != 0);
       }
     };
     auto issue_pv = [&](int t, int x) {  // O_x += P_x(t) V_t
-      const uint32_t sv = smem_u32(smem + AttnSmem::V_OFF + (t % AT_KST) * AT_KV_BYTES);
-      const uint32_t tp = tmem_base + x * 128 + (t & 1) * AT_N;  // P_x: 32 columns of packed bf16 pairs
-      const uint32_t to = tmem_base + 256 + x * AT_D;
+      const uint32_t sv = smem_u32(smem + AttnSmem::V_OFF + (t & 1) * AT_TILE_BYTES);
+      const uint32_t tp = tmem_base + x * AT_N;        // P_x: 64 columns of packed bf16 pairs
+      const uint32_t to = tmem_base + 256 + x * AT_D;  // O_x
 #pragma unroll
       for (int kk = 0; kk < AT_N / 16; ++kk)
-        mma_bf16_ts(to, tp + kk * 8, sdesc_mnmajor_sw128(sv + kk * 16 * 128, AT_KVHALF), IDESC_O, (t | kk) != 0);
+        mma_bf16_ts(to, tp + kk * 8, sdesc_mnmajor_sw128(sv + kk * 16 * 128, AT_HALF), IDESC_O, (t | kk) != 0);
     };
     mbar_wait(q_full, 0);
-    for (int t = 0; t < min(2, n_tiles); ++t) {
-      mbar_wait(&k_full[t % AT_KST], (t / AT_KST) & 1);
+    if (n_tiles > 0) {
+      mbar_wait(&k_full[0], 0);
       tc_fence_after();
       if (elect_one()) {
-        issue_s(t, 0);
-        mma_commit(&s_full[0 * 2 + (t & 1)]);
+        issue_s(0, 0);
+        mma_commit(&s_full[0]);
         if (two) {
-          issue_s(t, 1);
-          mma_commit(&s_full[1 * 2 + (t & 1)]);
+          issue_s(0, 1);
+          mma_commit(&s_full[1]);
         }
-        mma_commit(&k_empty[t % AT_KST]);
+        mma_commit(&k_empty[0]);
       }
       __syncwarp();
     }
     for (int j = 0; j < n_tiles; ++j) {
-      const bool more = j + 2 < n_tiles;
-      const int jb = j & 1;
-      // tile A: P_A(j) V_j, then S_A(j+2)
+      const bool more = j + 1 < n_tiles;
+      // tile A: P_A(j) V_j, then S_A(j+1)
       mbar_wait(&p_full[0], j & 1);
-      mbar_wait(&v_full[j % AT_KST], (j / AT_KST) & 1);
-      if (more) mbar_wait(&k_full[(j + 2) % AT_KST], ((j + 2) / AT_KST) & 1);
+      mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+      if (more) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
         issue_pv(j, 0);
-        mma_commit(&o_ready[0]);
         if (more) {
-          issue_s(j + 2, 0);
-          mma_commit(&s_full[0 * 2 + jb]);
+          issue_s(j + 1, 0);
+          mma_commit(&s_full[0]);
         }
         if (!two) {
-          mma_commit(&v_empty[j % AT_KST]);
-          if (more) mma_commit(&k_empty[(j + 2) % AT_KST]);
+          mma_commit(&v_empty[j & 1]);
+          if (more) mma_commit(&k_empty[(j + 1) & 1]);
         }
       }
       __syncwarp();
       if (two) {
-        // tile B: P_B(j) V_j, then S_B(j+2)
+        // tile B: P_B(j) V_j, then S_B(j+1)
         mbar_wait(&p_full[1], j & 1);
         tc_fence_after();
         if (elect_one()) {
           issue_pv(j, 1);
-          mma_commit(&o_ready[1]);
-          mma_commit(&v_empty[j % AT_KST]);
+          mma_commit(&v_empty[j & 1]);
           if (more) {
-            issue_s(j + 2, 1);
-            mma_commit(&s_full[1 * 2 + jb]);
-            mma_commit(&k_empty[(j + 2) % AT_KST]);
+            issue_s(j + 1, 1);
+            mma_commit(&s_full[1]);
+            mma_commit(&k_empty[(j + 1) & 1]);
           }
         }
         __syncwarp();
@@ -392,13 +379,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     }
     if (elect_one()) mma_commit(o_done);
     __syncwarp();
-  } else {
+  } else if (warp >= 4) {
     // ------------------------------------------------ softmax warpgroups
-    const int x = (warp - 2) / 4;        // Q tile: 0 = A (warps 2-5), 1 = B (warps 6-9)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(AT_REG_SOFTMAX));
+    const int x = (warp - 4) / 4;        // Q tile: 0 = A (warps 4-7), 1 = B (warps 8-11)
     const int quarter = warp & 3;        // TMEM lane quarter accessible to this warp
     const int r = quarter * 32 + lane;   // row within the Q tile == TMEM lane
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const uint32_t t_s0 = tmem_base + lane_base + x * 128;
+    const uint32_t t_s = tmem_base + lane_base + x * AT_N;
     const uint32_t t_o = tmem_base + lane_base + 256 + x * AT_D;
     const float sc = p.scale_log2;
     float m_run = -INFINITY, l_run = 0.0f;
@@ -408,21 +396,29 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const bool active = x == 0 || two;
     for (int j = 0; j < (active ? n_tiles : 0); ++j, cs.next()) {
       const int nvalid = cs.cur_valid();
-      const uint32_t t_s = t_s0 + (j & 1) * AT_N;
-      mbar_wait(&s_full[x * 2 + (j & 1)], (j >> 1) & 1);
+      mbar_wait(&s_full[x], j & 1);
       tc_fence_after();
-      uint32_t s[AT_N];
+      uint32_t s[128];
       tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
       tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+      tmem_ld32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
+      tmem_ld32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
       tmem_ld_wait();
       if (nvalid < AT_N) {  // ragged segment tail (warp-uniform)
 #pragma unroll
-        for (int i = 0; i < AT_N; ++i)
+        for (int i = 0; i < 128; ++i)
           if (i >= nvalid) s[i] = __float_as_uint(-INFINITY);
       }
-      float mx = __uint_as_float(s[0]);
+      // row max as a tree: 8 independent 3-input max chains, then 8 -> 1
+      float mq[8];
 #pragma unroll
-      for (int i = 1; i < AT_N; ++i) mx = fmaxf(mx, __uint_as_float(s[i]));
+      for (int k = 0; k < 8; ++k) mq[k] = fmaxf(__uint_as_float(s[k]), __uint_as_float(s[k + 8]));
+#pragma unroll
+      for (int i = 16; i < 128; i += 16)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mq[k] = fmaxf(mq[k], fmaxf(__uint_as_float(s[i + k]), __uint_as_float(s[i + 8 + k])));
+      const float mx = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
+                             fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
       const float m_tile = mx * sc;
       float alpha = 1.0f;
       bool rescale = false;
@@ -440,9 +436,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       // Pairs go through the packed fp32x2 FMA pipe (FFMA2/FADD2); 3 of
       // every 8 pairs take the polynomial exp2, the rest MUFU.EX2.
       const uint64_t sc2 = f32x2(sc, sc), nm2 = f32x2(-m_run, -m_run);
-      uint64_t rs2a = f32x2(0.f, 0.f), rs2b = rs2a;
+      uint64_t rs2[4];
 #pragma unroll
-      for (int i = 0; i < AT_N; i += 2) {
+      for (int k = 0; k < 4; ++k) rs2[k] = f32x2(0.f, 0.f);
+      uint32_t* pk = s;  // packed P overwrites the consumed front of s in place
+#pragma unroll
+      for (int i = 0; i < 128; i += 2) {
         const bool poly = ((i >> 1) & 7) >= 5;
         const uint64_t a = ffma2(f32x2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sc2, nm2);
         uint64_t e;
@@ -453,24 +452,19 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           unpack_f32x2(a, a0, a1);
           e = f32x2(ex2(a0), ex2(a1));
         }
-        if ((i >> 1) & 1)
-          rs2b = fadd2(rs2b, e);
-        else
-          rs2a = fadd2(rs2a, e);
+        rs2[(i >> 1) & 3] = fadd2(rs2[(i >> 1) & 3], e);
         float e0, e1;
         unpack_f32x2(e, e0, e1);
-        s[i / 2] = pack_bf16(e0, e1);  // packed P overwrites the consumed front of s
+        pk[i / 2] = pack_bf16(e0, e1);
       }
-      float r0, r1, r2, r3;
-      unpack_f32x2(rs2a, r0, r1);
-      unpack_f32x2(rs2b, r2, r3);
-      l_run = l_run * alpha + ((r0 + r1) + (r2 + r3));
-      tmem_st32_x(t_s, &s[0]);
+      float r[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) unpack_f32x2(rs2[k], r[2 * k], r[2 * k + 1]);
+      l_run = l_run * alpha + (((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7])));
+      tmem_st32_x(t_s + 0, &s[0]);
+      tmem_st32_x(t_s + 32, &s[32]);
       if (rescale) {
-        // O_x must not be mid-accumulation: wait for P(j-1).V, then scale;
-        // P(j).V is only issued after this warpgroup arrives on p_full
-        mbar_wait(&o_ready[x], (j - 1) & 1);
-        tc_fence_after();
+        // P(j-1).V is complete (implied by s_full(j)); O_x is idle until p_full(j)
 #pragma unroll 1
         for (int c0 = 0; c0 < AT_D; c0 += 32) {
           uint32_t v[32];
@@ -483,57 +477,52 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       }
       tmem_st_wait();
       tc_fence_before();
-      // S(j+1) is usually ready already, so a fast warp could arrive for
-      // tile j+1 before its siblings arrived for tile j and complete phase j
-      // early: arrive for j only once phase j-1 has completed
-      if (j > 0) mbar_wait(&p_full[x], (j - 1) & 1);
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[x]);
     }
     // epilogue: O / l -> bf16 (whole unit) or unnormalised (O, m, l) partials
     if (active) {
-      mbar_wait(o_done, 0);
-      tc_fence_after();
-      const int row = q0 + x * AT_M + r;
-      if (piece >= 0) {
-        const int64_t slot = (int64_t)(blockIdx.x - p.n_whole) * (2 * AT_M) + x * AT_M + r;
-        float* po = p.part_o + slot * AT_D;
+    mbar_wait(o_done, 0);
+    tc_fence_after();
+    const int row = q0 + x * AT_M + r;
+    if (piece >= 0) {
+      const int64_t slot = (int64_t)(blockIdx.x - p.n_whole) * (2 * AT_M) + x * AT_M + r;
+      float* po = p.part_o + slot * AT_D;
 #pragma unroll 1
-        for (int c0 = 0; c0 < AT_D; c0 += 32) {
-          uint32_t v[32];
-          if (n_tiles > 0) {
-            tmem_ld32(t_o + c0, v);
-            tmem_ld_wait();
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0u;
-          }
-          float4* o = reinterpret_cast<float4*>(po + c0);
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            o[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                               __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-        }
-        reinterpret_cast<float2*>(p.part_ml)[slot] = make_float2(n_tiles > 0 ? m_run : -INFINITY, l_run);
-      } else {
-        const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
-#pragma unroll 1
-        for (int c0 = 0; c0 < AT_D; c0 += 32) {
-          uint32_t v[32];
+      for (int c0 = 0; c0 < AT_D; c0 += 32) {
+        uint32_t v[32];
+        if (n_tiles > 0) {
           tmem_ld32(t_o + c0, v);
           tmem_ld_wait();
-          if (row < p.n_q) {
-            uint4* o = reinterpret_cast<uint4*>(p.out + (int64_t)row * p.ldo + col0 + c0);
+        } else {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              o[q] = make_uint4(
-                  pack_bf16(__uint_as_float(v[8 * q]) * inv_l, __uint_as_float(v[8 * q + 1]) * inv_l),
-                  pack_bf16(__uint_as_float(v[8 * q + 2]) * inv_l, __uint_as_float(v[8 * q + 3]) * inv_l),
-                  pack_bf16(__uint_as_float(v[8 * q + 4]) * inv_l, __uint_as_float(v[8 * q + 5]) * inv_l),
-                  pack_bf16(__uint_as_float(v[8 * q + 6]) * inv_l, __uint_as_float(v[8 * q + 7]) * inv_l));
-          }
+          for (int i = 0; i < 32; ++i) v[i] = 0u;
         }
+        float4* o = reinterpret_cast<float4*>(po + c0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          o[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                             __uint_as_float(v[4 * q + 3]));
       }
+      reinterpret_cast<float2*>(p.part_ml)[slot] = make_float2(n_tiles > 0 ? m_run : -INFINITY, l_run);
+    } else {
+    const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
+#pragma unroll 1
+    for (int c0 = 0; c0 < AT_D; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(t_o + c0, v);
+      tmem_ld_wait();
+      if (row < p.n_q) {
+        uint4* o = reinterpret_cast<uint4*>(p.out + (int64_t)row * p.ldo + col0 + c0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          o[q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q]) * inv_l, __uint_as_float(v[8 * q + 1]) * inv_l),
+                            pack_bf16(__uint_as_float(v[8 * q + 2]) * inv_l, __uint_as_float(v[8 * q + 3]) * inv_l),
+                            pack_bf16(__uint_as_float(v[8 * q + 4]) * inv_l, __uint_as_float(v[8 * q + 5]) * inv_l),
+                            pack_bf16(__uint_as_float(v[8 * q + 6]) * inv_l, __uint_as_float(v[8 * q + 7]) * inv_l));
+      }
+    }
+    }
     }
   }
 
@@ -667,7 +656,7 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
   CUtensorMap tq, tk, tv;
   int rc = make_tmap_bf16_2d(&tq, a->q, (uint64_t)a->n_q, (uint64_t)d, (uint64_t)d, AT_M, 64);
   if (rc) return rc;
-  rc = make_tmap_bf16_2d(&tk, a->k_arena, (uint64_t)a->arena_rows, (uint64_t)d, (uint64_t)d, AT_N, 64);  // 64 keys
+  rc = make_tmap_bf16_2d(&tk, a->k_arena, (uint64_t)a->arena_rows, (uint64_t)d, (uint64_t)d, AT_N, 64);
   if (rc) return rc;
   rc = make_tmap_bf16_2d(&tv, a->v_arena, (uint64_t)a->arena_rows, (uint64_t)d, (uint64_t)d, AT_N, 64);
   if (rc) return rc;

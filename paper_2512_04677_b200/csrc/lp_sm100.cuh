@@ -36,10 +36,24 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifdef LP_DEBUG_HANG
+// Debug builds: a wait that spins ~10 s reports itself and traps.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint64_t n = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++n == (1ull << 27)) {
+      printf("LP_DEBUG_HANG block %d thread %d: mbarrier smem+0x%x parity %u\n", blockIdx.x, threadIdx.x,
+             (unsigned)(smem_u32(bar) & 0xFFFFF), parity);
+      __trap();
+    }
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+#endif
 
 // ---- TMA -------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
