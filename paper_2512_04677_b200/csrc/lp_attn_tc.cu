@@ -206,8 +206,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint64_t* v_full = bars + 5;   // [2]
   uint64_t* v_empty = bars + 7;  // [2]
   uint64_t* s_full = bars + 9;   // [2] per Q tile
-  uint64_t* p_full = bars + 11;  // [2] per Q tile
-  uint64_t* o_done = bars + 13;
+  uint64_t* p_full = bars + 11;  // [2] per Q tile: all of P(j) in TMEM
+  uint64_t* p_half = bars + 13;  // [2] per Q tile: keys [0, 64) of P(j) in TMEM (O rescaled)
+  uint64_t* o_done = bars + 15;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
   int* seg_row = reinterpret_cast<int*>(smem + AttnSmem::SEG_OFF);
   int* seg_len = seg_row + LP_MAX_SEG;
@@ -254,6 +255,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
+      mbar_init(&p_half[i], 4);
     }
     mbar_init(o_done, 1);
     fence_barrier_init();
@@ -319,12 +321,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                     kk != 0);
       }
     };
-    auto issue_pv = [&](int t, int x) {  // O_x += P_x(t) V_t
+    auto issue_pv = [&](int t, int x, int h) {  // O_x += P_x(t)[keys 64h..] V_t[64h..]
       const uint32_t sv = smem_u32(smem + AttnSmem::V_OFF + (t & 1) * AT_TILE_BYTES);
       const uint32_t tp = tmem_base + x * AT_N;        // P_x: 64 columns of packed bf16 pairs
       const uint32_t to = tmem_base + 256 + x * AT_D;  // O_x
 #pragma unroll
-      for (int kk = 0; kk < AT_N / 16; ++kk)
+      for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
         mma_bf16_ts(to, tp + kk * 8, sdesc_mnmajor_sw128(sv + kk * 16 * 128, AT_HALF), IDESC_O, (t | kk) != 0);
     };
     mbar_wait(q_full, 0);
@@ -344,13 +346,18 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     }
     for (int j = 0; j < n_tiles; ++j) {
       const bool more = j + 1 < n_tiles;
-      // tile A: P_A(j) V_j, then S_A(j+1)
-      mbar_wait(&p_full[0], j & 1);
+      // tile A: P_A(j) V_j in two key halves (the first overlaps the softmax
+      // of the second), then S_A(j+1)
+      mbar_wait(&p_half[0], j & 1);
       mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) issue_pv(j, 0, 0);
+      __syncwarp();
+      mbar_wait(&p_full[0], j & 1);
       if (more) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        issue_pv(j, 0);
+        issue_pv(j, 0, 1);
         if (more) {
           issue_s(j + 1, 0);
           mma_commit(&s_full[0]);
@@ -363,10 +370,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       __syncwarp();
       if (two) {
         // tile B: P_B(j) V_j, then S_B(j+1)
+        mbar_wait(&p_half[1], j & 1);
+        tc_fence_after();
+        if (elect_one()) issue_pv(j, 1, 0);
+        __syncwarp();
         mbar_wait(&p_full[1], j & 1);
         tc_fence_after();
         if (elect_one()) {
-          issue_pv(j, 1);
+          issue_pv(j, 1, 1);
           mma_commit(&v_empty[j & 1]);
           if (more) {
             issue_s(j + 1, 1);
@@ -440,31 +451,30 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 #pragma unroll
       for (int k = 0; k < 4; ++k) rs2[k] = f32x2(0.f, 0.f);
       uint32_t* pk = s;  // packed P overwrites the consumed front of s in place
+      auto exp_pairs = [&](int i0) {
 #pragma unroll
-      for (int i = 0; i < 128; i += 2) {
-        const bool poly = ((i >> 1) & 7) >= 5;
-        const uint64_t a = ffma2(f32x2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sc2, nm2);
-        uint64_t e;
-        if (poly) {
-          e = ex2_poly2(a);
-        } else {
-          float a0, a1;
-          unpack_f32x2(a, a0, a1);
-          e = f32x2(ex2(a0), ex2(a1));
+        for (int i = i0; i < i0 + 64; i += 2) {
+          const bool poly = ((i >> 1) & 7) >= 5;
+          const uint64_t a = ffma2(f32x2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sc2, nm2);
+          uint64_t e;
+          if (poly) {
+            e = ex2_poly2(a);
+          } else {
+            float a0, a1;
+            unpack_f32x2(a, a0, a1);
+            e = f32x2(ex2(a0), ex2(a1));
+          }
+          rs2[(i >> 1) & 3] = fadd2(rs2[(i >> 1) & 3], e);
+          float e0, e1;
+          unpack_f32x2(e, e0, e1);
+          pk[i / 2] = pack_bf16(e0, e1);
         }
-        rs2[(i >> 1) & 3] = fadd2(rs2[(i >> 1) & 3], e);
-        float e0, e1;
-        unpack_f32x2(e, e0, e1);
-        pk[i / 2] = pack_bf16(e0, e1);
-      }
-      float r[8];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) unpack_f32x2(rs2[k], r[2 * k], r[2 * k + 1]);
-      l_run = l_run * alpha + (((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7])));
+      };
+      // keys [0, 64): P columns [0, 32); O is rescaled before P(j).V starts
+      exp_pairs(0);
       tmem_st32_x(t_s + 0, &s[0]);
-      tmem_st32_x(t_s + 32, &s[32]);
       if (rescale) {
-        // P(j-1).V is complete (implied by s_full(j)); O_x is idle until p_full(j)
+        // P(j-1).V is complete (implied by s_full(j)); O_x is idle until p_half(j)
 #pragma unroll 1
         for (int c0 = 0; c0 < AT_D; c0 += 32) {
           uint32_t v[32];
@@ -475,6 +485,17 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           tmem_st32(t_o + c0, v);
         }
       }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_half[x]);
+      // keys [64, 128): P columns [32, 64)
+      exp_pairs(64);
+      float r[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) unpack_f32x2(rs2[k], r[2 * k], r[2 * k + 1]);
+      l_run = l_run * alpha + (((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7])));
+      tmem_st32_x(t_s + 32, &s[32]);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();

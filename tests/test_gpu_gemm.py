@@ -47,7 +47,7 @@ def _ab(m, k, n, seed=0):
 
 
 @pytest.mark.parametrize("m,k,n", [(128, 64, 256), (300, 256, 512), (4680 // 4, 512, 384), (77, 1024, 64),
-                                   (1, 512, 768), (1000, 128, 128)])
+                                   (1, 512, 768), (1000, 128, 128), (4680, 128, 13824)])
 def test_store_bf16_and_f32(m, k, n):
     a, w = _ab(m, k, n)
     ref = a.float() @ w.float().T
