@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
+    ap.add_argument("--history-sigma", type=float, default=0.0,
+                    help="history-noise sigma (config 4: corrupted cache views, device Philox noise)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N>1 (gloo lets several ranks share one GPU in tests)")
     return ap.parse_args()
@@ -203,6 +205,18 @@ def roofline(prof, kern, n_tok, n_kv):
             kern[tag]["flops_per_launch"] = fl
             kern[tag]["tflops"] = fl / (kern[tag]["avg_ms"] / 1e3) / 1e12
             kern[tag]["frac_of_peak"] = kern[tag]["tflops"] / peak_tf
+    # HBM-bound kernels: algorithmic bytes per launch / duration vs the measured copy bandwidth
+    hbm = peaks.get("hbm_gbs", 6545.6)
+    S = prof.tokens_per_frame
+    eb = 2  # bf16 arena / activations
+    bytes_ = {"norm_mod": n_tok * d * (4 + eb),                       # h fp32 in, xa bf16 out
+              "sink_refresh": prof.n_layers * S * d * (4 + eb),        # K only: fp32 raw in, rotated bf16 out
+              "history_noise": (n_kv - S - n_tok) * d * (eb + eb)}     # ring rows in, scratch rows out (one of K/V)
+    for tag, b in bytes_.items():
+        if tag in kern:
+            kern[tag]["bytes_per_launch"] = b
+            kern[tag]["gbs"] = b / (kern[tag]["avg_ms"] / 1e3) / 1e9
+            kern[tag]["frac_of_hbm"] = kern[tag]["gbs"] / hbm
     if "attention" not in kern:
         return None
     ach = kern["attention"]["tflops"]
@@ -239,7 +253,8 @@ def run_ours(args):
     prof = profile_for(args.config)
     T, Lc = 4, 4
     cfg = lp.EngineConfig(mode="sequential", steps=T, cache_capacity=Lc, frames_per_block=3, profile=prof,
-                          precision="bf16", devices=(dev,), device_inputs=True, blocks=1 << 20)
+                          precision="bf16", devices=(dev,), device_inputs=True, blocks=1 << 20,
+                          history_sigma=args.history_sigma)
     pipe = lp.StreamingPipeline(cfg)
     n_tok = 3 * prof.tokens_per_frame
     lat = prof.latent_dim
@@ -302,6 +317,7 @@ def run_ours(args):
         "dtype": "bf16", "data": "synthetic (device-RNG random-init weights, N(0,1) noise blocks)",
         "config": {"workload": workload(args.config), "steps_T": T, "cache_L": Lc, "tokens_per_block": n_tok,
                    "n_kv_steady": n_kv_steady, "parallelism": "1 GPU, T steps sequential (TPP stages collapsed)",
+                   "history_sigma": args.history_sigma,
                    "l2": "inputs (weights + KV rings) >> 126 MB L2; no flush needed",
                    "block_latency_ms": ms_step, "achieved_tflops": ach, "frac_of_sustained_peak": ach / peak_tf,
                    "frac_of_burst_peak": ach / burst_tf,

@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
               }
               e.x_out[idx] = __fadd_rn(e.x_in[idx], __fmul_rn(v[j], dt));
             }
+            __threadfence_system();  // x_out may be a peer's receive slot: visible before the ready flag
             continue;
           }
           if (p.epilogue == LP_EPI_RESID) {
@@ -371,9 +372,14 @@ int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
     return launch_gemm_tc<128>(a, p, st);
   }
   LP_CHECK_ARG(a->ldc % 4 == 0, "gemm_tc: ldc alignment");
-  // Widest tile that divides N.  (A 192-wide tile would turn FFN-up's 13.5
-  // waves into 18 full ones, but measured slower: 0.62 vs 0.51 ms.)
-  if (a->n % 256 == 0) return launch_gemm_tc<256>(a, p, st);
+  // Widest tile that divides N, unless halving it removes more than 10% of
+  // the makespan in whole waves (the 1.3B shape's N = 1536 GEMMs: 1.5 waves
+  // of 256-wide tiles vs 3 full waves of 128).  Narrower tiles read more
+  // operand bytes per FLOP, so small wave gains are not worth it (a 192-wide
+  // tile for FFN-up at 14B: 18 full waves instead of 13.5, measured slower).
+  const long tiles_m = (a->m + GBM - 1) / GBM, sms = std::max(1, num_sms());
+  auto makespan = [&](int bn) { return ((tiles_m * (a->n / bn) + sms - 1) / sms) * bn; };
+  if (a->n % 256 == 0 && !(makespan(128) * 10 < makespan(256) * 9)) return launch_gemm_tc<256>(a, p, st);
   if (a->n % 128 == 0) return launch_gemm_tc<128>(a, p, st);
   if (a->n % 64 == 0) return launch_gemm_tc<64>(a, p, st);
   return fail(LP_EUNSUPPORTED, "gemm_tc: n must be a multiple of 64");

@@ -172,18 +172,23 @@ __global__ void sink_refresh_kernel(const float* __restrict__ kraw, const float*
   }
   RopeTab rt{desc->sink_cos, desc->sink_sin, geom};
   T* ko = karena + (int64_t)row * d + head * hd;
-  for (int p = lane; p < hd / 2; p += 32) {
-    const float2 t = *reinterpret_cast<const float2*>(k + 2 * p);
-    float x = t.x, y = t.y;
+  // 4 consecutive elements (2 rotary pairs) per lane: one 16-byte load, one
+  // 8-byte (bf16) store
+  for (int c = lane * 4; c < hd; c += 128) {
+    const float4 t = *reinterpret_cast<const float4*>(k + c);
+    float v[4] = {t.x, t.y, t.z, t.w};
     if (qk_norm) {
-      x = x * inv * (g_k ? g_k[head * hd + 2 * p] : 1.0f);
-      y = y * inv * (g_k ? g_k[head * hd + 2 * p + 1] : 1.0f);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = v[e] * inv * (g_k ? g_k[head * hd + c + e] : 1.0f);
     }
-    float c, s, xo, yo;
-    rt.get(tok, p, c, s);
-    rotate_pair(x, y, c, s, xo, yo);
-    ko[2 * p] = from_f32<T>(xo);
-    ko[2 * p + 1] = from_f32<T>(yo);
+    float o[4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      float cs, sn;
+      rt.get(tok, c / 2 + q, cs, sn);
+      rotate_pair(v[2 * q], v[2 * q + 1], cs, sn, o[2 * q], o[2 * q + 1]);
+    }
+    store4(ko + c, o);
   }
   if (vraw == nullptr) return;  // V rows are position-independent: written once per sink content
   vraw += layer * raw_stride;
@@ -229,6 +234,7 @@ __global__ void unpatchify_euler_kernel(const float* __restrict__ x, const float
     vv = v[t * pd + e];
   }
   xo[i] = __fadd_rn(x[i], __fmul_rn(vv, dt));
+  __threadfence_system();  // xo may be a peer's receive slot (fused TPP send)
 }
 
 // ------------------------------------------------------------------- RNG ---
@@ -276,7 +282,38 @@ __global__ void randn_kernel(T* out, int64_t n, uint64_t seed, uint64_t stream, 
 
 // History noise over the descriptor's history segments (kvcache.py:121-137):
 // dst rows = src rows + z * sigma (noise*sigma rounded, then the add).
-// Grid: x covers max history rows * d / 4 elements (packed over segments).
+// Grid: x covers max history rows * d / 4 elements (packed over segments);
+// each thread moves 4 contiguous elements with one vector load / store.
+// Device noise (perf runs) is Philox4x32-10 + Box-Muller on the fast
+// intrinsics (__logf, __sincosf); parity runs pass the reference's draws.
+__device__ __forceinline__ float4 normal4_fast(uint64_t seed, uint64_t stream, uint64_t ctr) {
+  uint4 c = make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream, (uint32_t)(stream >> 32));
+  uint2 k = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  uint4 r = Philox::gen(c, k);
+  const float inv = 2.3283064365386963e-10f;  // 2^-32
+  const float u0 = (r.x + 0.5f) * inv, u1 = (r.y + 0.5f) * inv, u2 = (r.z + 0.5f) * inv, u3 = (r.w + 0.5f) * inv;
+  const float r0 = sqrtf(-2.0f * __logf(u0)), r1 = sqrtf(-2.0f * __logf(u2));
+  float s0, c0, s1, c1;
+  __sincosf(6.283185307179586f * u1, &s0, &c0);
+  __sincosf(6.283185307179586f * u3, &s1, &c1);
+  return make_float4(r0 * c0, r0 * s0, r1 * c1, r1 * s1);
+}
+
+template <typename T>
+__device__ __forceinline__ void load4(const T* p, float* v);
+template <>
+__device__ __forceinline__ void load4<float>(const float* p, float* v) {
+  const float4 t = *reinterpret_cast<const float4*>(p);
+  v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
+}
+template <>
+__device__ __forceinline__ void load4<__nv_bfloat16>(const __nv_bfloat16* p, float* v) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&u.x);
+  const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
+  v[0] = __low2float(a), v[1] = __high2float(a), v[2] = __low2float(b), v[3] = __high2float(b);
+}
+
 template <typename T>
 __global__ void history_noise_kernel(T* __restrict__ arena, int d, const float* __restrict__ noise,
                                      int n_layers, int layer, int kv, const lp_block_desc* __restrict__ desc) {
@@ -289,19 +326,23 @@ __global__ void history_noise_kernel(T* __restrict__ arena, int d, const float* 
     const int s = e + 1;
     const int64_t len = (int64_t)desc->seg_len[s] * d;
     if (i < base + len) {
-      const int64_t off = i - base;
+      const int64_t off = i - base;  // multiple of 4, len multiple of d (of 4): 4 elements in range
       T* dst = arena + (int64_t)desc->seg_row[s] * d + off;
       const T* src = arena + (int64_t)desc->src_row[s] * d + off;
       float z[4];
       if (noise) {
-        const float* zp = noise + ((((int64_t)e * 2 + kv) * n_layers + layer) * len) + off;
-        for (int j = 0; j < 4; ++j) z[j] = (off + j < len) ? zp[j] : 0.0f;
+        const float4 t = *reinterpret_cast<const float4*>(noise + ((((int64_t)e * 2 + kv) * n_layers + layer) * len) + off);
+        z[0] = t.x, z[1] = t.y, z[2] = t.z, z[3] = t.w;
       } else {
-        float4 g = normal4(desc->noise_key, ((uint64_t)(layer * 2 + kv) << 8) | (uint64_t)e, (uint64_t)(off >> 2));
-        z[0] = g.x; z[1] = g.y; z[2] = g.z; z[3] = g.w;
+        const float4 g =
+            normal4_fast(desc->noise_key, ((uint64_t)(layer * 2 + kv) << 8) | (uint64_t)e, (uint64_t)(off >> 2));
+        z[0] = g.x, z[1] = g.y, z[2] = g.z, z[3] = g.w;
       }
-      for (int j = 0; j < 4 && off + j < len; ++j)
-        dst[j] = from_f32<T>(__fadd_rn(to_f32(src[j]), __fmul_rn(z[j], sigma)));
+      float x[4], o[4];
+      load4<T>(src, x);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] = __fadd_rn(x[j], __fmul_rn(z[j], sigma));
+      store4<T>(dst, o);
       return;
     }
     base += len;

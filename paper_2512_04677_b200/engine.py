@@ -274,9 +274,43 @@ class Stage:
                 self.fw.launch(stream=self.stream)
             self.graph = g
 
-    def forward(self, i: int, timed: bool = True) -> None:
-        """Enqueue the forward of block i (descriptor already staged)."""
+    def ensure_out_graphs(self, out_ptrs) -> None:
+        """Capture one forward graph per destination address of x' (TPP: the
+        peer-mapped receive slots of the next stage, so the velocity-head /
+        Euler epilogue stores straight over NVLink)."""
+        self.out_graphs = getattr(self, "out_graphs", {})
+        for ptr in out_ptrs:
+            if ptr in self.out_graphs:
+                continue
+            with torch.cuda.device(self.device):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream, capture_error_mode="thread_local"):
+                    self.fw.launch(stream=self.stream, x_out=int(ptr))
+                self.out_graphs[ptr] = g
+
+    def forward(self, i: int, timed: bool = True, out_ptr: int | None = None) -> None:
+        """Enqueue the forward of block i (descriptor already staged); with
+        ``out_ptr`` the final latent goes to that device address instead of
+        ``fw.x_out``."""
         fw = self.fw
+        if out_ptr is not None:
+            with torch.cuda.device(self.device):
+                e0 = torch.cuda.Event(enable_timing=True) if timed else None
+                e1 = torch.cuda.Event(enable_timing=True) if timed else None
+                if timed:
+                    e0.record(self.stream)
+                g = getattr(self, "out_graphs", {}).get(out_ptr)
+                if self.use_graph and g is not None:
+                    with torch.cuda.stream(self.stream):
+                        g.replay()
+                else:
+                    fw.launch(stream=self.stream, x_out=int(out_ptr))
+                if timed:
+                    e1.record(self.stream)
+                    self.ev.append((i, e0, e1))
+            self.nfe += 1
+            self.ring.push(i)
+            return
         with torch.cuda.device(self.device):
             e0 = torch.cuda.Event(enable_timing=True) if timed else None
             e1 = torch.cuda.Event(enable_timing=True) if timed else None

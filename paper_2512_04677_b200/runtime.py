@@ -287,7 +287,7 @@ class Forward:
                 self.arena.v[:, :S].copy_(self.v_raw)
 
     # ---------------------------------------------------------- forward ------
-    def launch(self, stream=None, x_out: torch.Tensor | None = None) -> None:
+    def launch(self, stream=None, x_out=None) -> None:
         """Enqueue the whole block forward + Euler step on ``stream``.
         Reads x_in / inbuf, writes vel, x_out (default self.x_out) and the
         current block's K/V rows of the arena."""
@@ -296,6 +296,7 @@ class Forward:
         N, d, f, nl = self.n_tokens, prof.model_dim, prof.ffn_dim, prof.n_layers
         ldt = dw.ldt
         xo = self.x_out if x_out is None else x_out
+        xo_ptr = xo if isinstance(xo, int) else xo.data_ptr()  # an int is a (peer-mapped) device address
         # conditioning row (denoiser.py:178-185)
         L.call("lp_cond_row", self.audio_ptr if self.audio_present else None, prof.audio_dim,
                dw.w_audio.data_ptr(), self.prompt_ptr, prof.prompt_dim, dw.w_prompt.data_ptr(), self.tau_ptr, 8,
@@ -316,10 +317,12 @@ class Forward:
         else:
             L.call("lp_add_row", self.x_in.data_ptr(), self.c.data_ptr(), self.h.data_ptr(), N, d, st)
         # sink K/V at i + delta for every layer (kvcache.py:86-90)
+        self._tag("sink_refresh", "begin", stream)
         L.call("lp_sink_refresh", self.k_raw.data_ptr(), None if self.sink_v_static else self.v_raw.data_ptr(),
                prof.tokens_per_frame, d,
                prof.n_heads, int(prof.qk_norm), _p(dw.g_k), prof.eps, self.desc_ptr, C.byref(self.geom),
                ar.k.data_ptr(), ar.v.data_ptr(), ldt, nl, prof.tokens_per_frame * d, ar.layer_stride, st)
+        self._tag("sink_refresh", "end", stream)
         esz = ar.k.element_size()
         norm_mode = 2 if prof.adaln else (1 if prof.pre_ln else 0)
         for l in range(nl):
@@ -328,8 +331,10 @@ class Forward:
             mods = self.mods[l] if prof.adaln else None
             mp = (lambda k: mods.data_ptr() + k * d * 4) if prof.adaln else (lambda k: 0)
             # pre-attention norm / modulation
+            self._tag("norm_mod", "begin", stream)
             L.call("lp_norm_mod", self.h.data_ptr(), N, d, norm_mode, prof.eps, mp(0) or None, mp(1) or None,
                    self.xa.data_ptr(), ldt, st)
+            self._tag("norm_mod", "end", stream)
             epi = L.QkvEpi(d, prof.n_heads, prof.head_dim, int(prof.qk_norm), prof.eps,
                            _p(dw.g_q[l]) if prof.qk_norm else 0, _p(dw.g_k[l]) if prof.qk_norm else 0,
                            self.q.data_ptr(), kl, vl, self.desc_ptr, self.geom)
@@ -346,8 +351,10 @@ class Forward:
             # history noise into the scratch rows (corrupted view)
             if self._sigma_on:
                 for kv, base in ((0, kl), (1, vl)):
+                    self._tag("history_noise", "begin", stream)
                     L.call("lp_history_noise", base, ldt, d, _p(self.noise), nl, l, kv, self.desc_ptr,
                            ar.hist_max * N, st)
+                    self._tag("history_noise", "end", stream)
             args = L.AttnArgs(ldt, N, prof.n_heads, prof.head_dim, self.scale, self.q.data_ptr(), kl, vl,
                               self.att.data_ptr(), self.desc_ptr, ar.rows, self.max_keys(), _p(self.attn_ws),
                               self.attn_ws_bytes)
@@ -362,8 +369,10 @@ class Forward:
                        gate=mp(2))
             if self.probe:
                 self.probe("o_proj", "end", stream)
+            self._tag("norm_mod", "begin", stream)
             L.call("lp_norm_mod", self.h.data_ptr(), N, d, norm_mode, prof.eps, mp(3) or None, mp(4) or None,
                    self.xa.data_ptr(), ldt, st)
+            self._tag("norm_mod", "end", stream)
             if self.probe:
                 self.probe("ffn_up", "begin", stream)
             self._proj(st, self.xa.data_ptr(), N, d, dw.w1[l], f, self.act.data_ptr(), f,
@@ -389,14 +398,14 @@ class Forward:
             if prof.patched:
                 L.call("lp_unpatchify_euler", self.x_in.data_ptr(), self.vel.data_ptr(), self.n_frames,
                        prof.channels, prof.height, prof.width, prof.patch[0], prof.patch[1], self.desc_ptr,
-                       xo.data_ptr(), st)
+                       xo_ptr, st)
             else:
                 L.call("lp_unpatchify_euler", self.x_in.data_ptr(), self.vel.data_ptr(), 1, 1, 1, N * d, 0, 0,
-                       self.desc_ptr, xo.data_ptr(), st)
+                       self.desc_ptr, xo_ptr, st)
         else:
             # velocity head with the flow step fused into the GEMM epilogue (K6)
             ph, pw = prof.patch if prof.patched else (0, 0)
-            self._euler = L.EulerEpi(self.x_in.data_ptr(), xo.data_ptr(), prof.channels, prof.height, prof.width,
+            self._euler = L.EulerEpi(self.x_in.data_ptr(), xo_ptr, prof.channels, prof.height, prof.width,
                                      ph, pw, self.desc_ptr)
             args = L.GemmArgs()
             args.in_dtype, args.out_dtype, args.epilogue = self.dw.ldt, L.LP_F32, L.EPI_EULER
@@ -407,6 +416,10 @@ class Forward:
             L.call("lp_gemm", C.byref(args), st)
 
     _sigma_on = False
+
+    def _tag(self, tag: str, phase: str, stream) -> None:
+        if self.probe:
+            self.probe(tag, phase, stream)
     # bf16: fuse the flow step into the velocity-head GEMM epilogue (engine
     # stages); the drop-in denoiser needs the raw velocity and turns it off
     fuse_euler = True

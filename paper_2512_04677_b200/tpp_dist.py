@@ -10,11 +10,14 @@ Reference -> B200 mapping:
 * ``_Link`` (engine.py:342-388), a bounded ``queue.Queue`` carrying only the
   ``LatentBlock`` -> ``IpcLink``: ``capacity`` latent slots + ready/free
   counters in the CONSUMER's HBM, mapped into the producer's process with
-  CUDA IPC; the producer's side stream copies x' into the slot over NVLink
-  and publishes ``ready`` with a system-scope release (lp_link_send), the
-  consumer's stream waits on it on the device (lp_link_recv) -- no host round
-  trip per block, and sequence numbers keep the FIFO invariant
-  (engine.py:360-363, :383-387);
+  CUDA IPC.  Default (fused) send: the producer's last step writes x'
+  straight into the consumer's slot from the velocity-head GEMM's Euler
+  epilogue (NVLink stores), after a device wait on the slot's ``free``
+  counter, then publishes ``ready`` with a system-scope release; fallback:
+  a side-stream copy kernel (lp_link_send) overlapped with the next block.
+  The consumer's stream waits on ``ready`` on the device (lp_link_recv) --
+  no host round trip per block, and sequence numbers keep the FIFO
+  invariant (engine.py:360-363, :383-387);
 * decoder thread (engine.py:465-480) -> the last rank of a pipeline, which
   reads each final latent back, decodes, and after block 0 performs the
   one-shot AAS and broadcasts the sink to the pipeline's ranks
@@ -265,6 +268,7 @@ class DeviceBackend:
         self.sendbuf = torch.zeros((2,) + self.shape, dtype=torch.float32, device=f"cuda:{device}")
         self.sent = [None, None]
         self._keep = None
+        self.fused = None  # (link, slot addresses): x' stored by the Euler epilogue into the peer's slots
 
     @property
     def x_in(self) -> torch.Tensor:
@@ -291,14 +295,35 @@ class DeviceBackend:
         with torch.cuda.stream(self.stream):
             self.x_in.copy_(x.reshape(self.x_in.shape), non_blocking=True)
 
+    def setup_fused_send(self, link: "IpcLink") -> None:
+        """Fuse the stage-boundary transfer into the last owned step: its
+        velocity-head GEMM's Euler epilogue stores x' straight into the
+        consumer's peer-mapped receive slot over NVLink (one captured graph
+        per slot); a device wait on the slot's ``free`` counter precedes the
+        forward and a system-scope release of ``ready`` follows it."""
+        slots = [link.peer[0] + s * link.nbytes for s in range(link.capacity)]
+        self.stages[-1].ensure_out_graphs(slots)
+        self.fused = (link, slots)
+
     def denoise(self, i: int, timed: bool = True) -> None:
         prev = None
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
-            for st in self.stages:
+            for n, st in enumerate(self.stages):
                 if prev is not None:
                     st.fw.x_in.copy_(prev.fw.x_out)
                 st.prepare(i)
-                st.forward(i, timed=timed)
+                if self.fused is not None and n == len(self.stages) - 1:
+                    link, slots = self.fused
+                    link._check(i)
+                    flags = link.peer[1]
+                    need = i + 1 - link.capacity
+                    if need > 0:  # slot i % capacity consumed by block i - capacity
+                        L.call("lp_wait", flags + 4, need, link.abort_ptr, link.timeout_ns, self.status.data_ptr(),
+                               self.stream.cuda_stream)
+                    st.forward(i, timed=timed, out_ptr=slots[i % link.capacity])
+                    L.call("lp_signal", flags, i + 1, self.stream.cuda_stream)
+                else:
+                    st.forward(i, timed=timed)
                 prev = st
 
     def send(self, link: IpcLink, i: int) -> None:
@@ -353,7 +378,7 @@ class DistTPP:
     streaming form used by bench.py."""
 
     def __init__(self, cfg: EngineConfig, rt=None, backend=None, transport: str = "ipc", device: int | None = None,
-                 rank: int | None = None, world: int | None = None):
+                 rank: int | None = None, world: int | None = None, fused_send: bool = True):
         if cfg.mode != "tpp":
             raise EngineConfigError(f"DistTPP needs mode 'tpp', got {cfg.mode!r}")
         self.rank = dist.get_rank() if rank is None else rank
@@ -368,6 +393,7 @@ class DistTPP:
             groups = [dist.new_group(list(r.ranks)) for r in self.roles if r.pos == 0]
             self.pipe_group = groups[self.role.pipe]
         self.transport = transport
+        self.fused_send = fused_send and transport == "ipc"
         if transport == "ipc":
             self.device = torch.cuda.current_device() if device is None else device
             L.init_device(self.device)
@@ -417,6 +443,8 @@ class DistTPP:
                 self.peer_aborts.append(_ipc_open(*every[r]["abort"]))
                 self._abort_handles.append(every[r]["abort"][0])
         self.backend.capture()  # graphs before any link kernel is in flight
+        if self.fused_send and self.link_out is not None:
+            self.backend.setup_fused_send(self.link_out)
         torch.cuda.synchronize(dev)
         dist.barrier()
 
@@ -487,7 +515,8 @@ class DistTPP:
             self._recv(i)
         self.backend.denoise(i)
         if not self.role.last:
-            self._send(i)
+            if not (self.fused_send and self.backend.fused is not None):
+                self._send(i)
             return None
         if out is not None and i != 0:
             self.backend.read_output(out)

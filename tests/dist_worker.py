@@ -118,10 +118,11 @@ def main():
         dev = int(os.environ.get("LP_TEST_DEVICE", "0"))
         torch.cuda.set_device(dev)
         prec = kw.pop("precision", "fp32")
+        fused = bool(kw.pop("fused", 1))
         if kw.pop("profile", None) == "wan_small":
             kw["profile"] = wan_small()
         cfg = lp.EngineConfig(mode="tpp", precision=prec, devices=(dev,), **kw)
-        res = tpp_dist.run_tpp_dist(cfg, transport="ipc", device=dev)
+        res = tpp_dist.run_tpp_dist(cfg, transport="ipc", device=dev, fused_send=fused)
         role = tpp_dist.pipeline_layout(world, cfg.steps)[rank]
     if res is not None:
         lat = np.stack([np.asarray(b.values, np.float32) for b in res.blocks])

@@ -133,3 +133,27 @@ def test_full_shape_tail_split_matches_reference(heads):
         assert rel_l2(tc[:, h * 128:(h + 1) * 128].float().cpu(), ref.cpu()) < 1e-2, h
     tc2 = _run("lp_attention", q, karena, varena, desc, heads, scale, n_kv)
     assert torch.equal(tc, tc2)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_device_history_noise_moments(dtype):
+    # kvcache.py:121-137 with the device Philox stream (perf runs): the
+    # corrupted view = ring + sigma * N(0,1) in the scratch rows, ring
+    # untouched; moments as the reference checks them (tests/test_kvcache.py:178-194)
+    d, n_tok, rows = 512, 300, 2400
+    sigma = 0.3
+    arena = torch.zeros((rows, d), dtype=dtype, device=DEV)
+    arena[0:n_tok] = 1.0  # ring slot contents
+    desc = make_desc(4, [(2000, 8), (1200, n_tok), (2100, 8)], 2100, 8, 128)
+    desc.src_row[1] = 0  # corrupted copy of ring rows [0, n_tok) into scratch rows [1200, +n_tok)
+    desc.sigma = sigma
+    desc.noise_key = 12345
+    ddev = upload_desc(desc)
+    ldt = L.LP_F32 if dtype == torch.float32 else L.LP_BF16
+    L.call("lp_history_noise", arena.data_ptr(), ldt, d, None, 1, 0, 0, ddev.data_ptr(), n_tok,
+           torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    z = (arena[1200:1200 + n_tok].float() - 1.0) / sigma
+    assert abs(float(z.mean())) < 0.02
+    assert abs(float(z.std()) - 1.0) < 0.05
+    assert torch.all(arena[0:n_tok] == 1.0)  # stored ring untouched

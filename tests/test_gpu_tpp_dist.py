@@ -19,11 +19,13 @@ from dist_worker import wan_small
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("nproc,name", [(2, "c1"), (4, "c1_sigma")])
-def test_ipc_tpp_fp32_equals_sequential(tmp_path, nproc, name):
+@pytest.mark.parametrize("nproc,name,fused", [(2, "c1", 1), (4, "c1_sigma", 1), (2, "c1_L1", 0)])
+def test_ipc_tpp_fp32_equals_sequential(tmp_path, nproc, name, fused):
+    # fused: x' stored into the peer slot by the last step's Euler epilogue;
+    # 0: side-stream copy kernel (lp_link_send)
     kw = dict(META[name]["kw"])
     out = tmp_path / "res"
-    launch(nproc, "gpu", out, dict(kw, link_timeout_s=60.0), timeout=600)
+    launch(nproc, "gpu", out, dict(kw, link_timeout_s=60.0, fused=fused), timeout=600)
     got = np.load(f"{out}.0.npy")
     seq = lp.run_sequential(lp.EngineConfig(mode="sequential", **kw))
     assert got.tobytes() == np.stack([b.values for b in seq.blocks]).tobytes()
