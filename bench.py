@@ -210,7 +210,8 @@ def roofline(prof, kern, n_tok, n_kv):
     S = prof.tokens_per_frame
     eb = 2  # bf16 arena / activations
     bytes_ = {"norm_mod": n_tok * d * (4 + eb),                       # h fp32 in, xa bf16 out
-              "sink_refresh": prof.n_layers * S * d * (4 + eb),        # K only: fp32 raw in, rotated bf16 out
+              "sink_refresh": prof.n_layers * S * prof.n_heads * (prof.axes[0] // 2) * (8 + 2 * eb)
+              + (prof.n_layers * S * prof.n_heads * 4 if prof.qk_norm else 0),  # temporal pairs: fp32 in, bf16 out
               "history_noise": (n_kv - S - n_tok) * d * (eb + eb)}     # ring rows in, scratch rows out (one of K/V)
     for tag, b in bytes_.items():
         if tag in kern:

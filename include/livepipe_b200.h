@@ -216,7 +216,19 @@ LP_API int lp_sink_refresh(const float* k_raw, const float* v_raw, int s_tokens,
                     int n_heads, int qk_norm, const float* g_k, float eps,
                     const lp_block_desc* desc, const lp_rope_geom* geom,
                     void* k_arena, void* v_arena, int arena_dtype, int n_layers,
-                    int64_t raw_layer_stride, int64_t arena_layer_stride, void* stream);
+                    int64_t raw_layer_stride, int64_t arena_layer_stride,
+                    float* inv_rms_out, void* stream);
+/* Per-block sink refresh of the TEMPORAL rotary pairs only (pairs
+   [0, geom->t_pairs) of every head; the spatial pairs and V do not depend on
+   the sink position i + delta and were written by lp_sink_refresh once per
+   sink content, which also stored the per-(layer, token, head) RMSNorm
+   factors in inv_rms [n_layers, S, n_heads] (qk_norm only; NULL otherwise).
+   Bitwise the same K rows as a full lp_sink_refresh at this position.      */
+LP_API int lp_sink_refresh_temporal(const float* k_raw, const float* inv_rms, int s_tokens, int d,
+                    int n_heads, int qk_norm, const float* g_k,
+                    const lp_block_desc* desc, const lp_rope_geom* geom, void* k_arena,
+                    int arena_dtype, int n_layers, int64_t raw_layer_stride,
+                    int64_t arena_layer_stride, void* stream);
 /* out[i] = silu(x[i]) cast to out_dtype (AdaLN input, wan profile)         */
 LP_API int lp_silu(const float* x, void* out, int n, int out_dtype, void* stream);
 /* QKV post-processing for the SIMT path (the tcgen05 GEMM fuses this into its

@@ -79,7 +79,9 @@ _SIGS = {
     "lp_add_row": ([vp, vp, vp, C.c_int, C.c_int, vp], C.c_int),
     "lp_norm_mod": ([vp, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp, vp, C.c_int, vp], C.c_int),
     "lp_sink_refresh": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_float, vp,
-                         C.POINTER(RopeGeom), vp, vp, C.c_int, C.c_int, i64, i64, vp], C.c_int),
+                         C.POINTER(RopeGeom), vp, vp, C.c_int, C.c_int, i64, i64, vp, vp], C.c_int),
+    "lp_sink_refresh_temporal": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.POINTER(RopeGeom), vp,
+                                  C.c_int, C.c_int, i64, i64, vp], C.c_int),
     "lp_silu": ([vp, vp, C.c_int, C.c_int, vp], C.c_int),
     "lp_patchify": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
     "lp_unpatchify_euler": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp],

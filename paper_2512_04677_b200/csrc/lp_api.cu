@@ -29,7 +29,9 @@ int cond_row(const float*, int, const float*, const float*, int, const float*, c
 int add_row(const float*, const float*, float*, int, int, cudaStream_t);
 int norm_mod(const float*, int, int, int, float, const float*, const float*, void*, int, cudaStream_t);
 int sink_refresh(const float*, const float*, int, int, int, int, const float*, float, const lp_block_desc*,
-                 const lp_rope_geom&, void*, void*, int, int, int64_t, int64_t, cudaStream_t);
+                 const lp_rope_geom&, void*, void*, int, int, int64_t, int64_t, float*, cudaStream_t);
+int sink_refresh_temporal(const float*, const float*, int, int, int, int, const float*, const lp_block_desc*,
+                          const lp_rope_geom&, void*, int, int, int64_t, int64_t, cudaStream_t);
 int silu(const float*, void*, int, int, cudaStream_t);
 int patchify(const float*, int, int, int, int, int, int, void*, int, cudaStream_t);
 int unpatchify_euler(const float*, const float*, int, int, int, int, int, int, const lp_block_desc*, float*,
@@ -146,10 +148,20 @@ int lp_norm_mod(const float* h, int rows, int d, int mode, float eps, const floa
 int lp_sink_refresh(const float* k_raw, const float* v_raw, int s_tokens, int d, int n_heads, int qk_norm,
                     const float* g_k, float eps, const lp_block_desc* desc, const lp_rope_geom* geom,
                     void* k_arena, void* v_arena, int arena_dtype, int n_layers, int64_t raw_layer_stride,
-                    int64_t arena_layer_stride, void* stream) {
+                    int64_t arena_layer_stride, float* inv_rms_out, void* stream) {
   LP_CHECK_ARG(k_raw && desc && geom && k_arena && v_arena, "lp_sink_refresh: null argument");
   return sink_refresh(k_raw, v_raw, s_tokens, d, n_heads, qk_norm, g_k, eps, desc, *geom, k_arena, v_arena,
-                      arena_dtype, n_layers, raw_layer_stride, arena_layer_stride, S(stream));
+                      arena_dtype, n_layers, raw_layer_stride, arena_layer_stride, inv_rms_out, S(stream));
+}
+
+int lp_sink_refresh_temporal(const float* k_raw, const float* inv_rms, int s_tokens, int d, int n_heads,
+                             int qk_norm, const float* g_k, const lp_block_desc* desc, const lp_rope_geom* geom,
+                             void* k_arena, int arena_dtype, int n_layers, int64_t raw_layer_stride,
+                             int64_t arena_layer_stride, void* stream) {
+  LP_CHECK_ARG(k_raw && desc && geom && k_arena, "lp_sink_refresh_temporal: null argument");
+  LP_CHECK_ARG(!qk_norm || inv_rms, "lp_sink_refresh_temporal: qk_norm needs inv_rms");
+  return sink_refresh_temporal(k_raw, inv_rms, s_tokens, d, n_heads, qk_norm, g_k, desc, *geom, k_arena,
+                               arena_dtype, n_layers, raw_layer_stride, arena_layer_stride, S(stream));
 }
 
 int lp_silu(const float* x, void* out, int n, int out_dtype, void* stream) {

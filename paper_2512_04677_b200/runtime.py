@@ -154,6 +154,7 @@ class Forward:
         self.k_raw = torch.zeros((prof.n_layers, S, d), dtype=fp, device=dev)
         self.v_raw = torch.zeros((prof.n_layers, S, d), dtype=fp, device=dev)
         self.sink_key = None
+        self.sink_inv = torch.zeros((prof.n_layers, S, prof.n_heads), dtype=fp, device=dev) if prof.qk_norm else None
         # rotary geometry
         t_dim, dh, dw_ = prof.axes
         self.t_dim = t_dim
@@ -281,10 +282,14 @@ class Forward:
                        w_col0=2 * d)
         self._sink_tmp = (sh, xs)
         if self.sink_v_static:
-            # V rows of the sink do not depend on the position: write them once
-            # per sink content (arena rows [0, S)); the per-block refresh is K only
-            with torch.cuda.stream(s_obj):
-                self.arena.v[:, :S].copy_(self.v_raw)
+            # V and the spatial rotary pairs of K do not depend on the sink
+            # position: one full refresh per sink content (arena rows [0, S),
+            # also storing the per-head RMS factors); the per-block refresh
+            # (captured in the graph) rotates the temporal pairs only
+            ar = self.arena
+            L.call("lp_sink_refresh", self.k_raw.data_ptr(), self.v_raw.data_ptr(), S, d, prof.n_heads,
+                   int(prof.qk_norm), _p(dw.g_k), prof.eps, self.desc_ptr, C.byref(self.geom), ar.k.data_ptr(),
+                   ar.v.data_ptr(), dw.ldt, prof.n_layers, S * d, ar.layer_stride, _p(self.sink_inv), st)
 
     # ---------------------------------------------------------- forward ------
     def launch(self, stream=None, x_out=None) -> None:
@@ -318,10 +323,15 @@ class Forward:
             L.call("lp_add_row", self.x_in.data_ptr(), self.c.data_ptr(), self.h.data_ptr(), N, d, st)
         # sink K/V at i + delta for every layer (kvcache.py:86-90)
         self._tag("sink_refresh", "begin", stream)
-        L.call("lp_sink_refresh", self.k_raw.data_ptr(), None if self.sink_v_static else self.v_raw.data_ptr(),
-               prof.tokens_per_frame, d,
-               prof.n_heads, int(prof.qk_norm), _p(dw.g_k), prof.eps, self.desc_ptr, C.byref(self.geom),
-               ar.k.data_ptr(), ar.v.data_ptr(), ldt, nl, prof.tokens_per_frame * d, ar.layer_stride, st)
+        if self.sink_v_static:
+            L.call("lp_sink_refresh_temporal", self.k_raw.data_ptr(), _p(self.sink_inv), prof.tokens_per_frame, d,
+                   prof.n_heads, int(prof.qk_norm), _p(dw.g_k), self.desc_ptr, C.byref(self.geom), ar.k.data_ptr(),
+                   ldt, nl, prof.tokens_per_frame * d, ar.layer_stride, st)
+        else:
+            L.call("lp_sink_refresh", self.k_raw.data_ptr(), self.v_raw.data_ptr(), prof.tokens_per_frame, d,
+                   prof.n_heads, int(prof.qk_norm), _p(dw.g_k), prof.eps, self.desc_ptr, C.byref(self.geom),
+                   ar.k.data_ptr(), ar.v.data_ptr(), ldt, nl, prof.tokens_per_frame * d, ar.layer_stride, None,
+                   st)
         self._tag("sink_refresh", "end", stream)
         esz = ar.k.element_size()
         norm_mode = 2 if prof.adaln else (1 if prof.pre_ln else 0)
