@@ -631,6 +631,44 @@ def run_sequential(cfg: RolloutCfg, weights: Weights | None = None, mm=mm_pinned
     return blocks, (np.concatenate(frames) if frames else None), sink
 
 
+def run_clean_kv(cfg: RolloutCfg, weights: Weights | None = None, mm=mm_pinned, codec=True):
+    """Clean-cache baseline (engine.py:292-331): one unified cache (timestep
+    0) fed by an extra full-stack pass on each block's final latent at level
+    0 (cache_entry, denoiser.py:278-291); every step attends to it with the
+    level check lifted.  Returns (blocks, frames or None, nfe)."""
+    p = cfg.profile
+    w = weights if weights is not None else build_weights(cfg.weight_seed, p)
+    audio, prompt, ref = conditions(cfg)
+    cd = Codec(cfg.weight_seed, p.latent_dim, cfg.pixel_dim, cfg.upsample) if codec else None
+    dt = -1.0 / cfg.steps
+    unified = []
+    sink = ref.copy()
+    blocks, frames, nfe = [], [], 0
+    for i in range(cfg.blocks):
+        x = noise_block(cfg, i)
+        for j in range(cfg.steps, 0, -1):
+            sigma = cfg.history_sigma
+            if cfg.history_mode == "scaled" and j >= 1:
+                sigma = sigma * level(cfg.steps, j)
+            view = corrupt(unified, sigma, cfg.noise_seed, i, j)
+            vel, _ = dit_forward(p, w, cfg.steps, x, i, j, view, audio[i], prompt, sink, i + cfg.sink_delta, mm=mm,
+                                 require_same_timestep=False, max_entries=cfg.cache_capacity)
+            nfe += 1
+            x = euler(x, vel, dt)
+        _, entry = dit_forward(p, w, cfg.steps, x, i, 0, list(unified), audio[i], prompt, sink, i + cfg.sink_delta,
+                               mm=mm, require_same_timestep=False)
+        nfe += 1
+        push(unified, entry, cfg.cache_capacity)
+        blocks.append(x)
+        if cd is not None:
+            frames.append(cd.decode(x))
+            if i == 0:
+                sink = cd.encode(cd.decode(x)[0])
+        elif i == 0:
+            sink = x[0].copy()
+    return blocks, (np.concatenate(frames) if frames else None), nfe
+
+
 def latents_bytes(blocks) -> bytes:
     """LPD1 dump: magic + (D, F, M) as little-endian u32, then the blocks'
     fp32 frames row-major, block-ascending (harness.py:254-264)."""

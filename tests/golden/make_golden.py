@@ -52,6 +52,18 @@ def main() -> None:
         arrays[f"{name}_latents"] = np.stack([b.values for b in seq.blocks])
         arrays[f"{name}_frames"] = seq.frames
 
+    # 1b. clean-KV baseline rollouts (engine.py:292-331): unified cache fed by the
+    # extra cache_entry pass, NFE = (T+1) per block
+    for name, kw in {
+        "c1_clean": dict(steps=4, blocks=3),
+        "c1_clean_sigma": dict(steps=3, blocks=4, cache_capacity=2, history_sigma=0.2),
+    }.items():
+        res = lp.run_clean_kv(lp.EngineConfig(mode="clean_kv", **kw))
+        meta[name] = {"kw": kw, "latents_sha256": lp.latents_digest(res.blocks),
+                      "frames_sha256": lp.frames_digest(res.frames), "nfe": res.nfe}
+        arrays[f"{name}_latents"] = np.stack([b.values for b in res.blocks])
+        arrays[f"{name}_frames"] = res.frames
+
     # 2. single denoise_block calls with a history view (velocity + kv)
     w = build_weights(7)
     sched = lp.TimestepSchedule.uniform(4)

@@ -189,3 +189,15 @@ def test_measured_timeline_export(tmp_path):
     assert tuple(ev) == res.timeline and rec["nfe"] == 16
     q = lp.write_latents(str(tmp_path / "x.lpd"), res.blocks)
     np.testing.assert_array_equal(lp.read_latents(q), np.stack([b.values for b in res.blocks]))
+
+
+@pytest.mark.parametrize("name", ["c1_clean", "c1_clean_sigma"])
+def test_clean_kv_matches_reference(name):
+    # the clean-KV baseline (engine.py:292-331) through the
+    # drop-in B200Denoiser, fp32 validation mode, vs the reference's rollout
+    kw = META[name]["kw"]
+    res = lp.run_clean_kv(lp.EngineConfig(mode="clean_kv", **kw))
+    got = np.stack([b.values for b in res.blocks])
+    assert rel_l2(got, G[f"{name}_latents"]) < TOL_FP32
+    assert rel_l2(res.frames, G[f"{name}_frames"]) < TOL_FP32
+    assert res.nfe == META[name]["nfe"]

@@ -72,3 +72,12 @@ def test_visible_schedule_matches_window_rule():
         for i, vis in enumerate(sched):
             mask = O.visible_mask(i, cap)
             assert vis == [m for m in range(i) if mask[m]]
+
+
+@pytest.mark.parametrize("name", ["c1_clean", "c1_clean_sigma"])
+def test_clean_kv_digests_match_reference(name):
+    m = META[name]
+    blocks, frames, nfe = O.run_clean_kv(_cfg(m["kw"]))
+    assert hashlib.sha256(O.latents_bytes(blocks)).hexdigest() == m["latents_sha256"]
+    assert hashlib.sha256(frames.astype("<f4").tobytes()).hexdigest() == m["frames_sha256"]
+    assert nfe == m["nfe"]
