@@ -177,46 +177,6 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                                (int64_t)(cur + row) * e.d;
         RopeTab rt{e.desc->rope_cos, e.desc->rope_sin, e.geom};
         const float* g = section == 0 ? e.g_q : e.g_k;
-        if (hd == 128) {
-          // one head = 128 accumulator columns: all four TMEM loads in flight,
-          // one wait, the head kept in registers for the RMS and the rotation
-          for (int h0 = 0; h0 < BN; h0 += 128) {
-            uint32_t r[128];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              tmem_ld32(tbase + h0 + 32 * q, *reinterpret_cast<uint32_t(*)[32]>(&r[32 * q]));
-            tmem_ld_wait();
-            float inv = 1.0f;
-            if (section < 2 && e.qk_norm) {
-              float ss[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-              for (int j = 0; j < 128; ++j) ss[j & 7] = fmaf(__uint_as_float(r[j]), __uint_as_float(r[j]), ss[j & 7]);
-              inv = rsqrtf((((ss[0] + ss[1]) + (ss[2] + ss[3])) + ((ss[4] + ss[5]) + (ss[6] + ss[7]))) / hd + e.eps);
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float v[32];
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[32 * q + j]);
-              const int col = col0 + h0 + 32 * q;  // column within the section
-              if (section < 2) {
-                if (e.qk_norm) {
-#pragma unroll
-                  for (int j = 0; j < 32; ++j) v[j] *= g ? __ldg(g + col + j) * inv : inv;
-                }
-#pragma unroll
-                for (int j = 0; j < 32; j += 2) {
-                  float cs, sn, xo, yo;
-                  rt.get(row, 16 * q + j / 2, cs, sn);
-                  rotate_pair(v[j], v[j + 1], cs, sn, xo, yo);
-                  v[j] = xo;
-                  v[j + 1] = yo;
-                }
-              }
-              if (valid) store_row32(dst_base + col, LP_BF16, v);
-            }
-          }
-        } else
         for (int h0 = 0; h0 < BN; h0 += hd) {
           float inv = 1.0f;
           if (section < 2 && e.qk_norm) {
