@@ -379,7 +379,9 @@ int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
   // tile for FFN-up at 14B: 18 full waves instead of 13.5, measured slower).
   const long tiles_m = (a->m + GBM - 1) / GBM, sms = std::max(1, num_sms());
   auto makespan = [&](int bn) { return ((tiles_m * (a->n / bn) + sms - 1) / sms) * bn; };
-  if (a->n % 256 == 0 && !(makespan(128) * 10 < makespan(256) * 9)) return launch_gemm_tc<256>(a, p, st);
+  // (only for short K: with K = 8960 the 128-wide tile measured slower even at 3 vs 1.5 waves)
+  if (a->n % 256 == 0 && !(a->k <= 4096 && makespan(128) * 10 < makespan(256) * 9))
+    return launch_gemm_tc<256>(a, p, st);
   if (a->n % 128 == 0) return launch_gemm_tc<128>(a, p, st);
   if (a->n % 64 == 0) return launch_gemm_tc<64>(a, p, st);
   return fail(LP_EUNSUPPORTED, "gemm_tc: n must be a multiple of 64");
