@@ -73,6 +73,7 @@ class RankRole:
     ranks: tuple         # global ranks of this pipeline, stage order
     steps: tuple         # owned t_index values, descending (denoising order)
     stages: tuple        # owned stage numbers k (1-based, reference numbering)
+    decode: bool = False  # dedicated decode rank (the paper's "+1" VAE GPU): no steps
 
     @property
     def first(self) -> bool:
@@ -91,23 +92,34 @@ class RankRole:
         return None if self.last else self.ranks[self.pos + 1]
 
 
-def pipeline_layout(world: int, steps: int) -> list:
-    """RankRole for every rank.  P = min(world, T) ranks per pipeline, stage
-    k on pipeline position (k-1)*P // T, world // P pipelines."""
+def pipeline_layout(world: int, steps: int, decode_gpu: bool = False) -> list:
+    """RankRole for every rank.  P = min(world, T) DiT ranks per pipeline,
+    stage k on pipeline position (k-1)*P // T, world // P pipelines.  With
+    ``decode_gpu`` every pipeline has one more rank that only decodes, runs
+    the one-shot AAS and broadcasts the sink (the paper's 4 DiT + 1 VAE
+    layout); world must then be a multiple of P + 1."""
     if world < 1 or steps < 1:
         raise EngineConfigError("world and steps must be >= 1")
-    p = min(world, steps)
-    if world % p:
-        raise EngineConfigError(f"world size {world} is not a multiple of the pipeline depth {p} (T={steps})")
-    n_pipes = world // p
+    extra = 1 if decode_gpu else 0
+    if world < 1 + extra:
+        raise EngineConfigError(f"world size {world} too small for a pipeline with a decode rank")
+    p = min(world - extra, steps)
+    width = p + extra
+    if world % width:
+        raise EngineConfigError(f"world size {world} is not a multiple of the pipeline width {width} "
+                                f"({p} DiT ranks{' + 1 decode rank' if extra else ''}, T={steps})")
+    n_pipes = world // width
     roles = []
     for r in range(world):
-        pipe, pos = divmod(r, p)
+        pipe, pos = divmod(r, width)
+        ranks = tuple(range(pipe * width, pipe * width + width))
+        if pos == p:  # the decode rank
+            roles.append(RankRole(r, world, pipe, n_pipes, pos, ranks, (), (), True))
+            continue
         ks = tuple(k for k in range(1, steps + 1) if (k - 1) * p // steps == pos)
         if not ks:
             raise EngineConfigError(f"pipeline position {pos} owns no step (world {world}, T={steps})")
-        roles.append(RankRole(r, world, pipe, n_pipes, pos, tuple(range(pipe * p, pipe * p + p)),
-                              tuple(steps - k + 1 for k in ks), ks))
+        roles.append(RankRole(r, world, pipe, n_pipes, pos, ranks, tuple(steps - k + 1 for k in ks), ks))
     return roles
 
 
@@ -252,6 +264,50 @@ class DistTransport:
 # ---------------------------------------------------------------------------
 
 
+class DecodeBackend:
+    """The dedicated decode rank: receives each final latent over the link
+    into HBM and reads it back for the (host) decode; no denoising steps."""
+
+    def __init__(self, cfg: EngineConfig, device: int):
+        prof = cfg.model_profile
+        self.device = device
+        self.stream = torch.cuda.Stream(device)
+        self.shape = (cfg.frames_per_block, prof.latent_dim)
+        self.buf = torch.zeros(self.shape, dtype=torch.float32, device=f"cuda:{device}")
+        self.status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{device}")
+        self.stages = []
+        self.fused = None
+
+    def capture(self) -> None:
+        pass
+
+    def set_sink(self, content: np.ndarray) -> None:
+        pass
+
+    def denoise(self, i: int, timed: bool = True) -> None:
+        pass
+
+    def recv(self, link: "IpcLink", i: int) -> None:
+        link.recv(self.buf, self.stream, i, self.status)
+
+    def read_output(self, out: torch.Tensor | None = None) -> np.ndarray | None:
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            if out is not None:
+                out.copy_(self.buf.reshape(out.shape), non_blocking=True)
+                return None
+            host = self.buf.cpu()
+        st = int(self.status.item())
+        if st != 0:
+            raise PipelineInvariantError(f"decode link wait failed with status {st}")
+        return host.numpy().copy()
+
+    def nfe(self) -> int:
+        return 0
+
+    def sync(self) -> None:
+        torch.cuda.synchronize(self.device)
+
+
 class DeviceBackend:
     """The owned steps of one rank: one ``Stage`` per step on one stream,
     chained on the device (x_out of step j -> x_in of step j-1)."""
@@ -378,12 +434,13 @@ class DistTPP:
     streaming form used by bench.py."""
 
     def __init__(self, cfg: EngineConfig, rt=None, backend=None, transport: str = "ipc", device: int | None = None,
-                 rank: int | None = None, world: int | None = None, fused_send: bool = True):
+                 rank: int | None = None, world: int | None = None, fused_send: bool = True,
+                 decode_gpu: bool = False):
         if cfg.mode != "tpp":
             raise EngineConfigError(f"DistTPP needs mode 'tpp', got {cfg.mode!r}")
         self.rank = dist.get_rank() if rank is None else rank
         self.world = dist.get_world_size() if world is None else world
-        self.roles = pipeline_layout(self.world, cfg.steps)
+        self.roles = pipeline_layout(self.world, cfg.steps, decode_gpu)
         self.role = self.roles[self.rank]
         self.seed = pipe_noise_seed(cfg, self.role.pipe)
         cfg = _with_seed(cfg, self.seed)
@@ -398,8 +455,11 @@ class DistTPP:
             self.device = torch.cuda.current_device() if device is None else device
             L.init_device(self.device)
             self.rt = rt or build_runtime(_with_devices(cfg, (self.device,)))
-            self.backend = backend or DeviceBackend(_with_devices(cfg, (self.device,)), self.rt, self.role,
-                                                    self.device)
+            if backend is None:
+                dcfg = _with_devices(cfg, (self.device,))
+                backend = (DecodeBackend(dcfg, self.device) if self.role.decode
+                           else DeviceBackend(dcfg, self.rt, self.role, self.device))
+            self.backend = backend
             self._setup_ipc()
         else:
             self.device = None

@@ -104,14 +104,15 @@ def main():
     from oracle import livepipe_oracle as O
 
     rank, world = dist.get_rank(), dist.get_world_size()
+    decode_gpu = bool(kw.pop("decode_gpu", 0))
     if mode == "cpu":
         cfg = lp.EngineConfig(mode="tpp", **kw)
-        role = tpp_dist.pipeline_layout(world, cfg.steps)[rank]
+        role = tpp_dist.pipeline_layout(world, cfg.steps, decode_gpu)[rank]
         seed = tpp_dist.pipe_noise_seed(cfg, role.pipe)
         import dataclasses
 
         be = OracleBackend(dataclasses.replace(cfg, noise_seed=seed), role)
-        res = tpp_dist.run_tpp_dist(cfg, backend=be, transport="dist")
+        res = tpp_dist.run_tpp_dist(cfg, backend=be, transport="dist", decode_gpu=decode_gpu)
     else:
         import torch
 
@@ -122,8 +123,8 @@ def main():
         if kw.pop("profile", None) == "wan_small":
             kw["profile"] = wan_small()
         cfg = lp.EngineConfig(mode="tpp", precision=prec, devices=(dev,), **kw)
-        res = tpp_dist.run_tpp_dist(cfg, transport="ipc", device=dev, fused_send=fused)
-        role = tpp_dist.pipeline_layout(world, cfg.steps)[rank]
+        res = tpp_dist.run_tpp_dist(cfg, transport="ipc", device=dev, fused_send=fused, decode_gpu=decode_gpu)
+        role = tpp_dist.pipeline_layout(world, cfg.steps, decode_gpu)[rank]
     if res is not None:
         lat = np.stack([np.asarray(b.values, np.float32) for b in res.blocks])
         rec = {"latents_sha256": hashlib.sha256(O.latents_bytes(list(lat))).hexdigest(), "nfe": res.nfe,

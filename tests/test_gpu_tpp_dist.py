@@ -40,3 +40,13 @@ def test_ipc_tpp_bf16_wan_equals_sequential(tmp_path):
     got = np.load(f"{out}.0.npy")
     seq = lp.run_sequential(lp.EngineConfig(mode="sequential", precision="bf16", profile=wan_small(), **kw))
     assert got.tobytes() == np.stack([b.values for b in seq.blocks]).tobytes()
+
+
+def test_ipc_tpp_with_decode_rank(tmp_path):
+    # the paper's DiT ranks + 1 decode rank layout (here 2 + 1 sharing one GPU)
+    kw = dict(META["c1"]["kw"])
+    out = tmp_path / "res"
+    launch(3, "gpu", out, dict(kw, link_timeout_s=60.0, decode_gpu=1), timeout=600)
+    got = np.load(f"{out}.0.npy")
+    seq = lp.run_sequential(lp.EngineConfig(mode="sequential", **kw))
+    assert got.tobytes() == np.stack([b.values for b in seq.blocks]).tobytes()

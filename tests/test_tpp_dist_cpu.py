@@ -53,6 +53,16 @@ def test_layouts():
     assert [r.steps for r in r3] == [(4, 3), (2,), (1,)]
     with pytest.raises(EngineConfigError):
         tpp_dist.pipeline_layout(6, 4)
+    # the paper's 4 DiT + 1 decode GPU layout, and two of them
+    r5 = tpp_dist.pipeline_layout(5, 4, decode_gpu=True)
+    assert [r.steps for r in r5] == [(4,), (3,), (2,), (1,), ()]
+    assert r5[4].decode and r5[4].last and r5[3].next_rank == 4 and not r5[3].last
+    r10 = tpp_dist.pipeline_layout(10, 4, decode_gpu=True)
+    assert [r.pipe for r in r10] == [0] * 5 + [1] * 5 and r10[9].decode
+    r3 = tpp_dist.pipeline_layout(3, 4, decode_gpu=True)
+    assert [r.steps for r in r3] == [(4, 3), (2, 1), ()]
+    with pytest.raises(EngineConfigError):
+        tpp_dist.pipeline_layout(7, 4, decode_gpu=True)
     # every step owned exactly once per pipeline
     for w in (1, 2, 3, 4, 8):
         for p in range(w // min(w, 4)):
@@ -86,3 +96,16 @@ def test_two_pipelines_stream_independent_content(tmp_path):
     ref1, _, _ = O.run_sequential(O.RolloutCfg(steps=2, blocks=3, noise_seed=tpp_dist.pipe_noise_seed(
         tpp_dist.EngineConfig(), 1)))
     np.testing.assert_array_equal(b, np.stack(ref1))
+
+
+@pytest.mark.parametrize("nproc,name", [(3, "c1"), (5, "c1_sigma")])
+def test_dedicated_decode_rank_matches_reference(tmp_path, nproc, name):
+    # DiT ranks + one decode rank that decodes, runs the one-shot AAS and
+    # broadcasts the sink; same rollout digests as the reference
+    m = META[name]
+    out = tmp_path / "res"
+    launch(nproc, "cpu", out, dict(m["kw"], decode_gpu=1))
+    rec = json.load(open(f"{out}.0"))
+    assert rec["latents_sha256"] == m["latents_sha256"]
+    assert rec["frames_sha256"] == m["frames_sha256"]
+    assert rec["nfe"] == m["nfe"]
