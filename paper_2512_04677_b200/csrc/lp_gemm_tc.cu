@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         for (int h0 = 0; h0 < BN; h0 += hd) {
           float inv = 1.0f;
           if (section < 2 && e.qk_norm) {
-            float ss = 0.0f;
+            float ss[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains, not one 128-long FMA chain
             for (int c0 = 0; c0 < hd; c0 += 32) {
               uint32_t r[32];
               tmem_ld32(tbase + h0 + c0, r);
@@ -188,10 +188,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
                 float v = __uint_as_float(r[j]);
-                ss += v * v;
+                ss[j & 3] = fmaf(v, v, ss[j & 3]);
               }
             }
-            inv = rsqrtf(ss / hd + e.eps);
+            inv = rsqrtf(((ss[0] + ss[1]) + (ss[2] + ss[3])) / hd + e.eps);
           }
           for (int c0 = 0; c0 < hd; c0 += 32) {
             uint32_t r[32];

@@ -394,6 +394,8 @@ int preload_rows() {
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, cond_row_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, add_row_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<float, 256>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<float, 128, 4>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<__nv_bfloat16, 128, 4>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<__nv_bfloat16, 256>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, sink_refresh_kernel<float>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, sink_refresh_kernel<__nv_bfloat16>));
@@ -427,11 +429,18 @@ int norm_mod(const float* h, int rows, int d, int mode, float eps, const float* 
   LP_CHECK_ARG(mode == 0 || d % 4 == 0, "norm_mod: d must be a multiple of 4");
   LP_CHECK_ARG(mode != 2 || (shift && scale), "norm_mod: modulation needs shift and scale");
   if (rows == 0) return LP_OK;
-  if (out_dtype == LP_BF16)
+  if (d <= 2048) {  // narrow rows (1.3B: d = 1536): 128 threads, 4 float4 per thread
+    if (out_dtype == LP_BF16)
+      norm_mod_kernel<__nv_bfloat16, 128, 4><<<rows, 128, 0, st>>>(h, d, mode, eps, shift, scale,
+                                                                   (__nv_bfloat16*)out);
+    else
+      norm_mod_kernel<float, 128, 4><<<rows, 128, 0, st>>>(h, d, mode, eps, shift, scale, (float*)out);
+  } else if (out_dtype == LP_BF16) {
     norm_mod_kernel<__nv_bfloat16, 256><<<rows, 256, 0, st>>>(h, d, mode, eps, shift, scale,
                                                                (__nv_bfloat16*)out);
-  else
+  } else {
     norm_mod_kernel<float, 256><<<rows, 256, 0, st>>>(h, d, mode, eps, shift, scale, (float*)out);
+  }
   return launch_status("norm_mod");
 }
 
