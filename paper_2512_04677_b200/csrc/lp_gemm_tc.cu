@@ -9,7 +9,8 @@
 //               128 x BN x 16 per instruction, accumulator in TMEM, double
 //               buffered (2 x BN columns) so the epilogue of tile t overlaps
 //               the main loop of tile t+1
-//   warps 2..5  epilogue: tcgen05.ld 32 rows x 32 columns per warp-load,
+//   warps 2..9  epilogue (two warps per TMEM lane quarter, one column half
+//               each): tcgen05.ld 32 rows x 32 columns per warp-load,
 //               fused STORE / RELU / GELU / gated RESIDUAL / QKV (per-head
 //               RMSNorm + rotary + scatter of k, v into the KV ring slot)
 #include <algorithm>
@@ -23,7 +24,7 @@ namespace lp {
 using namespace sm100;
 
 constexpr int GBM = 128, GBK = 64, GSTAGES = 4;
-constexpr int G_THREADS = 192;
+constexpr int G_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM lane quarter)
 
 struct GemmParams {
   int m, n, k;
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 8);
     }
     fence_barrier_init();
   }
@@ -152,8 +153,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       }
     }
   } else {
-    // ---------------- epilogue (warps 2..5) ----------------
+    // ---------------- epilogue (warps 2..9) ----------------
     const int quarter = warp & 3;  // TMEM lanes [32*quarter, +32) are addressable by this warp
+    const int half = (warp - 2) >> 2;  // the two warps of a lane quarter split the tile's columns
+    constexpr int HALF_N = BN / 2;
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int acc = local & 1;
@@ -177,7 +180,11 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                                (int64_t)(cur + row) * e.d;
         RopeTab rt{e.desc->rope_cos, e.desc->rope_sin, e.geom};
         const float* g = section == 0 ? e.g_q : e.g_k;
-        for (int h0 = 0; h0 < BN; h0 += hd) {
+        // one head per warp when the column half holds whole heads, else the
+        // half-0 warps take the whole tile
+        const bool split = HALF_N % hd == 0;
+        const int hb = split ? half * HALF_N : 0, he = split ? hb + HALF_N : (half ? 0 : BN);
+        for (int h0 = hb; h0 < he; h0 += hd) {
           float inv = 1.0f;
           if (section < 2 && e.qk_norm) {
             float ss[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains, not one 128-long FMA chain
@@ -223,7 +230,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           }
         }
       } else {
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = half * HALF_N; c0 < (half + 1) * HALF_N; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(tbase + c0, r);
           tmem_ld_wait();
