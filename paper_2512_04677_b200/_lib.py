@@ -12,6 +12,8 @@ import re
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+# LIVEPIPE_LIB points at an alternative build of the same ABI (kernel variant
+# sweeps, the LP_DEBUG_HANG build); default: the in-tree library
 LIB_PATH = os.environ.get("LIVEPIPE_LIB") or os.path.join(HERE, "liblivepipe_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "livepipe_b200.h")
 

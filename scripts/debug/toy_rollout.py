@@ -1,6 +1,6 @@
 import json, sys, os
 import numpy as np
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import paper_2512_04677_b200 as lp
 from oracle import livepipe_oracle as O
