@@ -49,9 +49,9 @@ using namespace sm100;
 constexpr int AT_M = 128;      // query rows per softmax warpgroup
 constexpr int AT_N = 128;      // keys per tile
 constexpr int AT_D = 128;      // head dim
-constexpr int AT_THREADS = 640;  // WG0: TMA warp, MMA warp, 2 idle; warps 4-11: softmax of Q tile A, 12-19: B
-constexpr int AT_REG_CTRL = 56;      // setmaxnreg budget of the control warpgroup
-constexpr int AT_REG_SOFTMAX = 104;  // ... and of each softmax warp (56*128 + 104*512 <= 640*96)
+constexpr int AT_THREADS = 384;  // WG0: TMA warp, MMA warp, 2 idle; WG1, WG2: softmax of Q tiles A, B
+constexpr int AT_REG_CTRL = 56;  // setmaxnreg budget of the control warpgroup
+constexpr int AT_REG_SOFTMAX = 224;  // ... and of each softmax warpgroup (56*128 + 224*256 <= 64K)
 constexpr int AT_TILE_BYTES = AT_N * AT_D * 2;  // 32 KB
 constexpr int AT_HALF = AT_TILE_BYTES / 2;      // one 64-column SW128 block
 constexpr float AT_RESCALE_THRESH = 8.0f;       // log2 units: rescale O when the max grows > 2^8
@@ -194,53 +194,6 @@ __device__ __forceinline__ void tmem_st32_x(uint32_t taddr, const uint32_t* r) {
       "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
 }
 
-// 16 TMEM lanes x 256 bits per repetition (tcgen05.ld.16x256b): thread t gets
-// lanes t/4 and t/4 + 8, columns 2*(t%4) + {0, 1} of each 8-column group.
-__device__ __forceinline__ void tmem_ld_16x256b_x16(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.16x256b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, "
-      "%36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, "
-      "%57, %58, %59, %60, %61, %62, %63}, [%64];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
-        "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
-        "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
-        "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
-        "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld_16x256b_x8(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_st_16x256b_x8(uint32_t taddr, const uint32_t* r) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
-}
-// 16 lanes x 128 bits per repetition: thread t writes lanes t/4, t/4 + 8 of
-// column t%4 of each 4-column group (r[2g], r[2g + 1]).
-__device__ __forceinline__ void tmem_st_16x128b_x8(uint32_t taddr, const uint32_t* r) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.16x128b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
-}
-
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
@@ -301,8 +254,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 8);
-      mbar_init(&p_half[i], 8);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_half[i], 4);
     }
     mbar_init(o_done, 1);
     fence_barrier_init();
@@ -438,24 +391,16 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     if (elect_one()) mma_commit(o_done);
     __syncwarp();
   } else if (warp >= 4) {
-    // ------------------------------------------------ softmax warps
-    // 8 warps per Q tile.  Warp (quarter, slab) owns TMEM lanes
-    // 32*quarter + 16*slab + [0, 16) through the 16x256b / 16x128b access
-    // shapes: thread t holds rows L = t/4 and L + 8 of its slab and, per
-    // 8-key group g, keys 8g + 2(t%4) + {0, 1}; the 4 threads of a row
-    // reduce its max with two shuffles, P goes back packed as exactly the
-    // 16x128b layout (P column 4g + t%4 = keys 8g + 2(t%4) + {0, 1}).
+    // ------------------------------------------------ softmax warpgroups
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(AT_REG_SOFTMAX));
-    const int x = (warp - 4) / 8;          // Q tile: 0 = A (warps 4-11), 1 = B (warps 12-19)
-    const int slab = ((warp - 4) / 4) & 1;  // 16-lane half of the warp's lane quarter
-    const int quarter = warp & 3;
-    const int q4 = lane & 3, L = lane >> 2;
-    const int lb = quarter * 32 + slab * 16;  // first TMEM lane of this warp's slab
-    const uint32_t lane_base = (uint32_t)lb << 16;
+    const int x = (warp - 4) / 4;        // Q tile: 0 = A (warps 4-7), 1 = B (warps 8-11)
+    const int quarter = warp & 3;        // TMEM lane quarter accessible to this warp
+    const int r = quarter * 32 + lane;   // row within the Q tile == TMEM lane
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t t_s = tmem_base + lane_base + x * AT_N;
     const uint32_t t_o = tmem_base + lane_base + 256 + x * AT_D;
     const float sc = p.scale_log2;
-    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};  // rows L, L + 8 (partial over 32 keys)
+    float m_run = -INFINITY, l_run = 0.0f;
     TileCursor cs;
     cs.init(seg_row, seg_len, n_seg_s[0]);
     cs.skip(t_first);
@@ -464,92 +409,80 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       const int nvalid = cs.cur_valid();
       mbar_wait(&s_full[x], j & 1);
       tc_fence_after();
-      uint32_t s[64];  // s[4g + v]: v = 0, 1 -> row L keys 8g + 2*q4 + v; v = 2, 3 -> row L + 8
-      tmem_ld_16x256b_x16(t_s, s);
+      uint32_t s[128];
+      tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+      tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+      tmem_ld32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
+      tmem_ld32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
       tmem_ld_wait();
       if (nvalid < AT_N) {  // ragged segment tail (warp-uniform)
 #pragma unroll
-        for (int g = 0; g < 16; ++g)
-#pragma unroll
-          for (int v = 0; v < 4; ++v)
-            if (8 * g + 2 * q4 + (v & 1) >= nvalid) s[4 * g + v] = __float_as_uint(-INFINITY);
+        for (int i = 0; i < 128; ++i)
+          if (i >= nvalid) s[i] = __float_as_uint(-INFINITY);
       }
-      float mx[2];
+      // row max as a tree: 8 independent 3-input max chains, then 8 -> 1
+      float mq[8];
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        float mq[4];
+      for (int k = 0; k < 8; ++k) mq[k] = fmaxf(__uint_as_float(s[k]), __uint_as_float(s[k + 8]));
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          mq[k] = fmaxf(__uint_as_float(s[4 * k + 2 * rr]), __uint_as_float(s[4 * k + 2 * rr + 1]));
+      for (int i = 16; i < 128; i += 16)
 #pragma unroll
-        for (int g = 4; g < 16; g += 4)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mq[k] = fmaxf(mq[k], fmaxf(__uint_as_float(s[4 * (g + k) + 2 * rr]),
-                                       __uint_as_float(s[4 * (g + k) + 2 * rr + 1])));
-        float m = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
-        mx[rr] = m * sc;
-      }
-      float alpha[2] = {1.0f, 1.0f};
+        for (int k = 0; k < 8; ++k) mq[k] = fmaxf(mq[k], fmaxf(__uint_as_float(s[i + k]), __uint_as_float(s[i + 8 + k])));
+      const float mx = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
+                             fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
+      const float m_tile = mx * sc;
+      float alpha = 1.0f;
       bool rescale = false;
       if (j == 0) {
-        m_run[0] = mx[0];
-        m_run[1] = mx[1];
+        m_run = m_tile;
       } else {
-        const bool need0 = mx[0] > m_run[0] + AT_RESCALE_THRESH, need1 = mx[1] > m_run[1] + AT_RESCALE_THRESH;
-        rescale = __any_sync(0xffffffffu, need0 || need1);
-        if (need0) {
-          alpha[0] = ex2(m_run[0] - mx[0]);
-          m_run[0] = mx[0];
-        }
-        if (need1) {
-          alpha[1] = ex2(m_run[1] - mx[1]);
-          m_run[1] = mx[1];
+        const bool need = m_tile > m_run + AT_RESCALE_THRESH;
+        rescale = __any_sync(0xffffffffu, need);
+        if (need) {
+          alpha = ex2(m_run - m_tile);
+          m_run = m_tile;
         }
       }
-      const uint64_t sc2 = f32x2(sc, sc);
-      const uint64_t nm2[2] = {f32x2(-m_run[0], -m_run[0]), f32x2(-m_run[1], -m_run[1])};
-      uint64_t rs2[2][2];
+      // p = 2^(s*scale*log2e - m), packed to bf16 pairs in key order.
+      // Pairs go through the packed fp32x2 FMA pipe (FFMA2/FADD2); 3 of
+      // every 8 pairs take the polynomial exp2, the rest MUFU.EX2.
+      const uint64_t sc2 = f32x2(sc, sc), nm2 = f32x2(-m_run, -m_run);
+      uint64_t rs2[4];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) rs2[0][k] = rs2[1][k] = f32x2(0.f, 0.f);
-      // exponentials of 8-key groups [g0, g1): packed P overwrites the front of s
-      auto exp_groups = [&](int g0, int g1) {
+      for (int k = 0; k < 4; ++k) rs2[k] = f32x2(0.f, 0.f);
+      uint32_t* pk = s;  // packed P overwrites the consumed front of s in place
+      auto exp_pairs = [&](int i0) {
 #pragma unroll
-        for (int g = g0; g < g1; ++g)
-#pragma unroll
-          for (int rr = 0; rr < 2; ++rr) {
-            const bool poly = ((2 * g + rr) & 7) >= 5;  // 3 of every 8 pairs on the FMA pipe
-            const uint64_t a =
-                ffma2(f32x2(__uint_as_float(s[4 * g + 2 * rr]), __uint_as_float(s[4 * g + 2 * rr + 1])), sc2, nm2[rr]);
-            uint64_t e;
-            if (poly) {
-              e = ex2_poly2(a);
-            } else {
-              float a0, a1;
-              unpack_f32x2(a, a0, a1);
-              e = f32x2(ex2(a0), ex2(a1));
-            }
-            rs2[rr][g & 1] = fadd2(rs2[rr][g & 1], e);
-            float e0, e1;
-            unpack_f32x2(e, e0, e1);
-            s[2 * g + rr] = pack_bf16(e0, e1);  // P(row L + 8rr, column 4g + q4)
+        for (int i = i0; i < i0 + 64; i += 2) {
+          const bool poly = ((i >> 1) & 7) >= 5;
+          const uint64_t a = ffma2(f32x2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sc2, nm2);
+          uint64_t e;
+          if (poly) {
+            e = ex2_poly2(a);
+          } else {
+            float a0, a1;
+            unpack_f32x2(a, a0, a1);
+            e = f32x2(ex2(a0), ex2(a1));
           }
+          rs2[(i >> 1) & 3] = fadd2(rs2[(i >> 1) & 3], e);
+          float e0, e1;
+          unpack_f32x2(e, e0, e1);
+          pk[i / 2] = pack_bf16(e0, e1);
+        }
       };
       // keys [0, 64): P columns [0, 32); O is rescaled before P(j).V starts
-      exp_groups(0, 8);
-      tmem_st_16x128b_x8(t_s, &s[0]);
+      exp_pairs(0);
+      tmem_st32_x(t_s + 0, &s[0]);
       if (rescale) {
         // P(j-1).V is complete (implied by s_full(j)); O_x is idle until p_half(j)
 #pragma unroll 1
-        for (int c0 = 0; c0 < AT_D; c0 += 64) {
-          uint32_t v[32];  // 16x256b.x8: columns [c0, c0 + 64) of rows L, L + 8
-          tmem_ld_16x256b_x8(t_o + c0, v);
+        for (int c0 = 0; c0 < AT_D; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(t_o + c0, v);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha[(i >> 1) & 1]);
-          tmem_st_16x256b_x8(t_o + c0, v);
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+          tmem_st32(t_o + c0, v);
         }
       }
       tmem_st_wait();
@@ -557,69 +490,60 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_half[x]);
       // keys [64, 128): P columns [32, 64)
-      exp_groups(8, 16);
-      tmem_st_16x128b_x8(t_s + 32, &s[16]);
+      exp_pairs(64);
+      float r[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) unpack_f32x2(rs2[k], r[2 * k], r[2 * k + 1]);
+      l_run = l_run * alpha + (((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7])));
+      tmem_st32_x(t_s + 32, &s[32]);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[x]);
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        float a0, a1, b0, b1;
-        unpack_f32x2(rs2[rr][0], a0, a1);
-        unpack_f32x2(rs2[rr][1], b0, b1);
-        l_run[rr] = l_run[rr] * alpha[rr] + ((a0 + a1) + (b0 + b1));
-      }
     }
-    // epilogue: O / l -> bf16 (whole unit) or unnormalised (O, m, l) partials;
-    // the row sum adds the 4 threads' partial sums
+    // epilogue: O / l -> bf16 (whole unit) or unnormalised (O, m, l) partials
     if (active) {
-      float lt[2];
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        float l = l_run[rr];
-        l += __shfl_xor_sync(0xffffffffu, l, 1);
-        l += __shfl_xor_sync(0xffffffffu, l, 2);
-        lt[rr] = l;
-      }
-      mbar_wait(o_done, 0);
-      tc_fence_after();
-      const int row0 = q0 + x * AT_M + lb + L;  // rows row0, row0 + 8
+    mbar_wait(o_done, 0);
+    tc_fence_after();
+    const int row = q0 + x * AT_M + r;
+    if (piece >= 0) {
+      const int64_t slot = (int64_t)(blockIdx.x - p.n_whole) * (2 * AT_M) + x * AT_M + r;
+      float* po = p.part_o + slot * AT_D;
 #pragma unroll 1
-      for (int c0 = 0; c0 < AT_D; c0 += 64) {
-        uint32_t v[32];  // v[4g' + 2rr + e]: row L + 8rr, column c0 + 8g' + 2*q4 + e
+      for (int c0 = 0; c0 < AT_D; c0 += 32) {
+        uint32_t v[32];
         if (n_tiles > 0) {
-          tmem_ld_16x256b_x8(t_o + c0, v);
+          tmem_ld32(t_o + c0, v);
           tmem_ld_wait();
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = 0u;
         }
+        float4* o = reinterpret_cast<float4*>(po + c0);
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          if (piece >= 0) {
-            const int64_t slot = (int64_t)(blockIdx.x - p.n_whole) * (2 * AT_M) + x * AT_M + lb + L + 8 * rr;
-            float* po = p.part_o + slot * AT_D + c0 + 2 * q4;
-#pragma unroll
-            for (int g = 0; g < 8; ++g)
-              *reinterpret_cast<float2*>(po + 8 * g) =
-                  make_float2(__uint_as_float(v[4 * g + 2 * rr]), __uint_as_float(v[4 * g + 2 * rr + 1]));
-            if (c0 == 0 && q4 == 0)
-              reinterpret_cast<float2*>(p.part_ml)[slot] =
-                  make_float2(n_tiles > 0 ? m_run[rr] : -INFINITY, lt[rr]);
-          } else {
-            const int row = row0 + 8 * rr;
-            const float inv_l = lt[rr] > 0.0f ? 1.0f / lt[rr] : 0.0f;
-            if (row < p.n_q) {
-              __nv_bfloat16* o = p.out + (int64_t)row * p.ldo + col0 + c0 + 2 * q4;
-#pragma unroll
-              for (int g = 0; g < 8; ++g)
-                *reinterpret_cast<uint32_t*>(o + 8 * g) = pack_bf16(__uint_as_float(v[4 * g + 2 * rr]) * inv_l,
-                                                                     __uint_as_float(v[4 * g + 2 * rr + 1]) * inv_l);
-            }
-          }
-        }
+        for (int q = 0; q < 8; ++q)
+          o[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                             __uint_as_float(v[4 * q + 3]));
       }
+      reinterpret_cast<float2*>(p.part_ml)[slot] = make_float2(n_tiles > 0 ? m_run : -INFINITY, l_run);
+    } else {
+    const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
+#pragma unroll 1
+    for (int c0 = 0; c0 < AT_D; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(t_o + c0, v);
+      tmem_ld_wait();
+      if (row < p.n_q) {
+        uint4* o = reinterpret_cast<uint4*>(p.out + (int64_t)row * p.ldo + col0 + c0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          o[q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q]) * inv_l, __uint_as_float(v[8 * q + 1]) * inv_l),
+                            pack_bf16(__uint_as_float(v[8 * q + 2]) * inv_l, __uint_as_float(v[8 * q + 3]) * inv_l),
+                            pack_bf16(__uint_as_float(v[8 * q + 4]) * inv_l, __uint_as_float(v[8 * q + 5]) * inv_l),
+                            pack_bf16(__uint_as_float(v[8 * q + 6]) * inv_l, __uint_as_float(v[8 * q + 7]) * inv_l));
+      }
+    }
+    }
     }
   }
 
