@@ -5,6 +5,7 @@ match the C compiler's."""
 import ctypes
 import os
 import subprocess
+import sys
 
 import pytest
 
@@ -52,3 +53,12 @@ def test_ops_fail_loudly_without_device():
         pytest.skip("GPU present")
     with pytest.raises(L.LivepipeError):
         L.call("lp_init", 0)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    # no CPU fallback: without the CUDA library every op raises
+    code = ("import paper_2512_04677_b200._lib as L\n"
+            "try:\n    L.load()\nexcept ImportError as e:\n    print('IMPORTERROR', e)\n")
+    env = dict(os.environ, LIVEPIPE_LIB=str(tmp_path / "missing.so"), PYTHONPATH=ROOT)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT)
+    assert "IMPORTERROR" in out.stdout and "no CPU fallback" in out.stdout
