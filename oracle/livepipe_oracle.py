@@ -21,7 +21,7 @@ The oracle never touches a GPU and is never imported by the product package.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field, replace
+from dataclasses import dataclass, field
 
 import numpy as np
 

@@ -20,7 +20,6 @@ sigma > 0 (kvcache.py:121-137; the ring itself is never modified).
 from __future__ import annotations
 
 import ctypes as C
-import math
 import threading
 import time
 

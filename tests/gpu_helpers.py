@@ -6,7 +6,7 @@ import numpy as np
 import torch
 
 from paper_2512_04677_b200 import _lib as L
-from paper_2512_04677_b200.numerics import rope_table, spatial_tables
+from paper_2512_04677_b200.numerics import rope_table
 
 
 def rel_l2(a, b) -> float:

@@ -9,7 +9,6 @@ import os
 
 import numpy as np
 import pytest
-import torch
 
 import paper_2512_04677_b200 as lp
 from oracle import livepipe_oracle as O

@@ -6,7 +6,6 @@ NVLink peers).  Results must equal the single-process sequential run
 bitwise (reference tests/test_acceptance.py:60-83)."""
 
 import json
-import os
 
 import numpy as np
 import pytest

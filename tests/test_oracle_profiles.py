@@ -5,10 +5,8 @@ geometry agree with the oracle's (CPU only)."""
 import dataclasses
 
 import numpy as np
-import pytest
 
 from oracle import livepipe_oracle as O
-import paper_2512_04677_b200 as lp
 from paper_2512_04677_b200.model import build_weights as pkg_build, ModelProfile
 
 
