@@ -14,6 +14,7 @@
 //               fused STORE / RELU / GELU / gated RESIDUAL / QKV (per-head
 //               RMSNorm + rotary + scatter of k, v into the KV ring slot)
 #include <algorithm>
+#include <cstdlib>
 
 #include "lp_common.cuh"
 #include "lp_sm100.cuh"
@@ -57,6 +58,155 @@ __device__ __forceinline__ void store_row32(void* out, int out_dtype, const floa
     float4* o = reinterpret_cast<float4*>(out);
 #pragma unroll
     for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+}
+
+// Epilogue of one accumulator tile for this thread's row: TMEM (tbase: lane
+// quarter + accumulator buffer) -> fused QKV / EULER / RESID / activation.
+// n0: first output column of the tile; half: which column half this warp
+// owns (two epilogue warps per TMEM lane quarter).
+template <int BN>
+__device__ __forceinline__ void gemm_epilogue_tile(const GemmParams& p, int row, bool valid, uint32_t tbase,
+                                                   int n0, int half, int lane) {
+  constexpr int HALF_N = BN / 2;
+  if (p.epilogue == LP_EPI_QKV) {
+    const lp_qkv_epi& e = p.qkv;
+    const int hd = e.head_dim;
+    const int section = n0 / e.d;  // 0 q, 1 k, 2 v
+    const int col0 = n0 - section * e.d;
+    int cur = e.desc->cur_row;
+    __nv_bfloat16* dst_base =
+        section == 0 ? reinterpret_cast<__nv_bfloat16*>(e.q_out) + (int64_t)row * e.d
+                     : reinterpret_cast<__nv_bfloat16*>(section == 1 ? e.k_arena : e.v_arena) +
+                           (int64_t)(cur + row) * e.d;
+    RopeTab rt{e.desc->rope_cos, e.desc->rope_sin, e.geom};
+    const float* g = section == 0 ? e.g_q : e.g_k;
+    // one head per warp when the column half holds whole heads, else the
+    // half-0 warps take the whole tile
+    const bool split = HALF_N % hd == 0;
+    const int hb = split ? half * HALF_N : 0, he = split ? hb + HALF_N : (half ? 0 : BN);
+    for (int h0 = hb; h0 < he; h0 += hd) {
+      float inv = 1.0f;
+      if (section < 2 && e.qk_norm) {
+        float ss[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains, not one 128-long FMA chain
+        for (int c0 = 0; c0 < hd; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tbase + h0 + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float v = __uint_as_float(r[j]);
+            ss[j & 3] = fmaf(v, v, ss[j & 3]);
+          }
+        }
+        inv = rsqrtf(((ss[0] + ss[1]) + (ss[2] + ss[3])) / hd + e.eps);
+      }
+      for (int c0 = 0; c0 < hd; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tbase + h0 + c0, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        const int col = col0 + h0 + c0;  // column within the section
+        if (section < 2) {
+          float cs[16], sn[16], gg[32];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) rt.get(row, c0 / 2 + j, cs[j], sn[j]);
+          if (e.qk_norm) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) gg[j] = g ? __ldg(g + col + j) * inv : inv;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= gg[j];
+          }
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            float xo, yo;
+            rotate_pair(v[j], v[j + 1], cs[j / 2], sn[j / 2], xo, yo);
+            v[j] = xo;
+            v[j + 1] = yo;
+          }
+        }
+        if (valid) store_row32(dst_base + col, LP_BF16, v);
+      }
+    }
+  } else {
+    for (int c0 = half * HALF_N; c0 < (half + 1) * HALF_N; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld32(tbase + c0, r);
+      tmem_ld_wait();
+      const int col = n0 + c0;
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+      if (!valid) continue;
+      if (p.epilogue == LP_EPI_EULER) {
+        const lp_euler_epi& e = p.euler;
+        const float dt = e.desc->dt;
+        int64_t base;
+        int gy = 0, gx = 0;
+        if (e.ph == 0) {
+          base = (int64_t)row * p.n;
+        } else {
+          const int hp = e.height / e.ph, wp = e.width / e.pw, tpf = hp * wp;
+          const int f = row / tpf, tok = row % tpf;
+          gy = tok / wp;
+          gx = tok % wp;
+          base = (int64_t)f * e.channels * e.height * e.width;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int c = col + j;
+          int64_t idx;
+          if (e.ph == 0) {
+            idx = base + c;
+          } else {
+            const int pp = e.ph * e.pw, ch = c / pp, py = (c % pp) / e.pw, px = c % e.pw;
+            idx = base + ((int64_t)ch * e.height + gy * e.ph + py) * e.width + gx * e.pw + px;
+          }
+          e.x_out[idx] = __fadd_rn(e.x_in[idx], __fmul_rn(v[j], dt));
+        }
+        __threadfence_system();  // x_out may be a peer's receive slot: visible before the ready flag
+        continue;
+      }
+      if (p.epilogue == LP_EPI_RESID) {
+        // all loads first (h and gate may alias as far as the compiler
+        // knows; interleaving loads with stores serialises DRAM round trips)
+        float4* h = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.c) + (int64_t)row * p.ldc + col);
+        float4 o[8], g[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] = __ldcs(h + q);
+        if (p.gate) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) g[q] = __ldg(reinterpret_cast<const float4*>(p.gate + col) + q);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) g[q] = make_float4(1.f, 1.f, 1.f, 1.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          o[q].x = fmaf(g[q].x, v[4 * q], o[q].x);
+          o[q].y = fmaf(g[q].y, v[4 * q + 1], o[q].y);
+          o[q].z = fmaf(g[q].z, v[4 * q + 2], o[q].z);
+          o[q].w = fmaf(g[q].w, v[4 * q + 3], o[q].w);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) __stcs(h + q, o[q]);
+      } else {
+        if (p.epilogue == LP_EPI_STORE && p.bias) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += p.bias[col + j];
+        } else if (p.epilogue == LP_EPI_RELU) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+        } else if (p.epilogue == LP_EPI_GELU) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = gelu_tanh_f(v[j]);
+        }
+        const int esz = p.out_dtype == LP_BF16 ? 2 : 4;
+        store_row32(reinterpret_cast<uint8_t*>(p.c) + ((int64_t)row * p.ldc + col) * esz, p.out_dtype, v);
+      }
+    }
   }
 }
 
@@ -156,7 +306,6 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     // ---------------- epilogue (warps 2..9) ----------------
     const int quarter = warp & 3;  // TMEM lanes [32*quarter, +32) are addressable by this warp
     const int half = (warp - 2) >> 2;  // the two warps of a lane quarter split the tile's columns
-    constexpr int HALF_N = BN / 2;
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int acc = local & 1;
@@ -168,145 +317,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       const bool valid = row < p.m;
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
 
-      if (p.epilogue == LP_EPI_QKV) {
-        const lp_qkv_epi& e = p.qkv;
-        const int hd = e.head_dim;
-        const int section = n0 / e.d;  // 0 q, 1 k, 2 v
-        const int col0 = n0 - section * e.d;
-        int cur = e.desc->cur_row;
-        __nv_bfloat16* dst_base =
-            section == 0 ? reinterpret_cast<__nv_bfloat16*>(e.q_out) + (int64_t)row * e.d
-                         : reinterpret_cast<__nv_bfloat16*>(section == 1 ? e.k_arena : e.v_arena) +
-                               (int64_t)(cur + row) * e.d;
-        RopeTab rt{e.desc->rope_cos, e.desc->rope_sin, e.geom};
-        const float* g = section == 0 ? e.g_q : e.g_k;
-        // one head per warp when the column half holds whole heads, else the
-        // half-0 warps take the whole tile
-        const bool split = HALF_N % hd == 0;
-        const int hb = split ? half * HALF_N : 0, he = split ? hb + HALF_N : (half ? 0 : BN);
-        for (int h0 = hb; h0 < he; h0 += hd) {
-          float inv = 1.0f;
-          if (section < 2 && e.qk_norm) {
-            float ss[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains, not one 128-long FMA chain
-            for (int c0 = 0; c0 < hd; c0 += 32) {
-              uint32_t r[32];
-              tmem_ld32(tbase + h0 + c0, r);
-              tmem_ld_wait();
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                float v = __uint_as_float(r[j]);
-                ss[j & 3] = fmaf(v, v, ss[j & 3]);
-              }
-            }
-            inv = rsqrtf(((ss[0] + ss[1]) + (ss[2] + ss[3])) / hd + e.eps);
-          }
-          for (int c0 = 0; c0 < hd; c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tbase + h0 + c0, r);
-            tmem_ld_wait();
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-            const int col = col0 + h0 + c0;  // column within the section
-            if (section < 2) {
-              float cs[16], sn[16], gg[32];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) rt.get(row, c0 / 2 + j, cs[j], sn[j]);
-              if (e.qk_norm) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) gg[j] = g ? __ldg(g + col + j) * inv : inv;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] *= gg[j];
-              }
-#pragma unroll
-              for (int j = 0; j < 32; j += 2) {
-                float xo, yo;
-                rotate_pair(v[j], v[j + 1], cs[j / 2], sn[j / 2], xo, yo);
-                v[j] = xo;
-                v[j + 1] = yo;
-              }
-            }
-            if (valid) store_row32(dst_base + col, LP_BF16, v);
-          }
-        }
-      } else {
-        for (int c0 = half * HALF_N; c0 < (half + 1) * HALF_N; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(tbase + c0, r);
-          tmem_ld_wait();
-          const int col = n0 + c0;
-          float v[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          if (!valid) continue;
-          if (p.epilogue == LP_EPI_EULER) {
-            const lp_euler_epi& e = p.euler;
-            const float dt = e.desc->dt;
-            int64_t base;
-            int gy = 0, gx = 0;
-            if (e.ph == 0) {
-              base = (int64_t)row * p.n;
-            } else {
-              const int hp = e.height / e.ph, wp = e.width / e.pw, tpf = hp * wp;
-              const int f = row / tpf, tok = row % tpf;
-              gy = tok / wp;
-              gx = tok % wp;
-              base = (int64_t)f * e.channels * e.height * e.width;
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int c = col + j;
-              int64_t idx;
-              if (e.ph == 0) {
-                idx = base + c;
-              } else {
-                const int pp = e.ph * e.pw, ch = c / pp, py = (c % pp) / e.pw, px = c % e.pw;
-                idx = base + ((int64_t)ch * e.height + gy * e.ph + py) * e.width + gx * e.pw + px;
-              }
-              e.x_out[idx] = __fadd_rn(e.x_in[idx], __fmul_rn(v[j], dt));
-            }
-            __threadfence_system();  // x_out may be a peer's receive slot: visible before the ready flag
-            continue;
-          }
-          if (p.epilogue == LP_EPI_RESID) {
-            // all loads first (h and gate may alias as far as the compiler
-            // knows; interleaving loads with stores serialises DRAM round trips)
-            float4* h = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.c) + (int64_t)row * p.ldc + col);
-            float4 o[8], g[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) o[q] = __ldcs(h + q);
-            if (p.gate) {
-#pragma unroll
-              for (int q = 0; q < 8; ++q) g[q] = __ldg(reinterpret_cast<const float4*>(p.gate + col) + q);
-            } else {
-#pragma unroll
-              for (int q = 0; q < 8; ++q) g[q] = make_float4(1.f, 1.f, 1.f, 1.f);
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              o[q].x = fmaf(g[q].x, v[4 * q], o[q].x);
-              o[q].y = fmaf(g[q].y, v[4 * q + 1], o[q].y);
-              o[q].z = fmaf(g[q].z, v[4 * q + 2], o[q].z);
-              o[q].w = fmaf(g[q].w, v[4 * q + 3], o[q].w);
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) __stcs(h + q, o[q]);
-          } else {
-            if (p.epilogue == LP_EPI_STORE && p.bias) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] += p.bias[col + j];
-            } else if (p.epilogue == LP_EPI_RELU) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
-            } else if (p.epilogue == LP_EPI_GELU) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = gelu_tanh_f(v[j]);
-            }
-            const int esz = p.out_dtype == LP_BF16 ? 2 : 4;
-            store_row32(reinterpret_cast<uint8_t*>(p.c) + ((int64_t)row * p.ldc + col) * esz, p.out_dtype, v);
-          }
-        }
-      }
+      gemm_epilogue_tile<BN>(p, row, valid, tbase, n0, half, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -319,6 +330,167 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, TMEM_COLS);
   }
+}
+
+// ---------------------------------------------------------------------------
+// 2-CTA variant (cluster pair, tcgen05.mma.cta_group::2): tile 256 x BN per
+// pair, each CTA loads its 128 rows of A and its BN/2 rows of B, the leader
+// issues M = 256 MMAs whose accumulator halves land in each CTA's TMEM.  Per
+// CTA a k-block costs 32 KB of shared memory instead of 48 KB, so 6 stages
+// buffer 1.5x more time against TMA latency.
+constexpr int G2_STAGES = 6;
+
+template <int BN>
+struct Gemm2Smem {
+  static constexpr int A_BYTES = GBM * GBK * 2;
+  static constexpr int B_BYTES = (BN / 2) * GBK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = G2_STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const GemmParams p) {
+  using SM = Gemm2Smem<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+  uint64_t* empty = full + G2_STAGES;
+  uint64_t* tfull = empty + G2_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const int tiles_m = (p.m + 2 * GBM - 1) / (2 * GBM), tiles_n = p.n / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = p.k / GBK;
+  const int cid = blockIdx.x >> 1, nclu = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < G2_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 16);  // 8 epilogue warps x 2 CTAs (the leader's copy is used)
+    }
+    fence_barrier_init();
+  }
+  cluster_sync_all();  // barriers initialised in both CTAs before any remote arrive / TMA
+  if (warp == 1) tmem_alloc_2cta(tmem_slot, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint64_t pol = l2_policy_evict_last();
+      for (int tile = cid; tile < num_tiles; tile += nclu) {
+        int m0 = (tile % tiles_m) * 2 * GBM + rank * GBM;
+        if (m0 >= p.m) m0 = p.m > GBM ? p.m - GBM : 0;  // wholly past M: load valid rows, results discarded
+        const int n0 = (tile / tiles_m) * BN + rank * (BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * SM::STAGE_BYTES;
+          uint8_t* sb = sa + SM::A_BYTES;
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * SM::STAGE_BYTES);
+          tma_load_2d_2sm(sa, &tmA, &full[stage], kb * GBK, m0, pol);
+          tma_load_2d_2sm(sb, &tmB, &full[stage], kb * GBK, n0, pol);
+          if (++stage == G2_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader only) ----------------
+    if (rank == 0) {
+      constexpr uint32_t IDESC = idesc_bf16_f32(2 * GBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int tile = cid; tile < num_tiles; tile += nclu, ++local) {
+        const int acc = local & 1;
+        const uint32_t aphase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = smem_u32(smem + stage * SM::STAGE_BYTES);
+            const uint32_t sb = sa + SM::A_BYTES;
+            const uint64_t da = sdesc_kmajor_sw128(sa), db = sdesc_kmajor_sw128(sb);
+#pragma unroll
+            for (int k = 0; k < GBK / 16; ++k)
+              mma_bf16_ss_2cta(d_tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), IDESC, (kb | k) != 0);
+            mma_commit_2cta_mc(&empty[stage]);
+            if (kb == num_kb - 1) mma_commit_2cta_mc(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == G2_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..9, both CTAs) ----------------
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    int local = 0;
+    for (int tile = cid; tile < num_tiles; tile += nclu, ++local) {
+      const int acc = local & 1;
+      const uint32_t aphase = (local >> 1) & 1;
+      const int m0 = (tile % tiles_m) * 2 * GBM + rank * GBM, n0 = (tile / tiles_m) * BN;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const int row = m0 + quarter * 32 + lane;
+      const bool valid = row < p.m;
+      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      gemm_epilogue_tile<BN>(p, row, valid, tbase, n0, half, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's smem / TMEM are in use until the leader's last MMA is consumed
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2cta(tmem_base, 2 * BN);
+  }
+}
+
+template <int BN>
+static int launch_gemm_tc2(const lp_gemm_args* a, const GemmParams& p, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  int rc = make_tmap_bf16_2d(&ta, a->a, (uint64_t)a->m, (uint64_t)a->k, (uint64_t)a->lda, GBM, GBK);
+  if (rc) return rc;
+  rc = make_tmap_bf16_2d(&tb, a->w, (uint64_t)a->n, (uint64_t)a->k, (uint64_t)a->ldw, BN / 2, GBK);
+  if (rc) return rc;
+  const int tiles = ((a->m + 2 * GBM - 1) / (2 * GBM)) * (a->n / BN);
+  const int clusters = std::min(tiles, std::max(1, num_sms() / 2));
+  const int smem = Gemm2Smem<BN>::TOTAL;
+  auto kern = gemm_tc2_kernel<BN>;
+  LP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<2 * clusters, G_THREADS, smem, st>>>(ta, tb, p);
+  return launch_status("gemm_tc2");
 }
 
 template <int BN>
@@ -342,8 +514,12 @@ int preload_gemm_tc() {
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, gemm_tc_kernel<64>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, gemm_tc_kernel<128>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, gemm_tc_kernel<256>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, gemm_tc2_kernel<256>));
   return LP_OK;
 }
+
+static bool g_gemm2 = getenv("LP_NO_GEMM2") == nullptr;      // LP_NO_GEMM2=1 forces 1-CTA tiles
+static bool g_gemm2_all = getenv("LP_GEMM2_ALL") != nullptr;  // LP_GEMM2_ALL=1: pairs whenever N % 256 == 0
 
 int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
   LP_CHECK_ARG(num_sms() > 0, "lp_init() must be called before the tcgen05 GEMM");
@@ -387,8 +563,14 @@ int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
   const long tiles_m = (a->m + GBM - 1) / GBM, sms = std::max(1, num_sms());
   auto makespan = [&](int bn) { return ((tiles_m * (a->n / bn) + sms - 1) / sms) * bn; };
   // (only for short K: with K = 8960 the 128-wide tile measured slower even at 3 vs 1.5 waves)
-  if (a->n % 256 == 0 && !(a->k <= 4096 && makespan(128) * 10 < makespan(256) * 9))
+  if (a->n % 256 == 0 && !(a->k <= 4096 && makespan(128) * 10 < makespan(256) * 9)) {
+    // cluster-pair (2-CTA) tiles unless their waves lose more than the ~8%
+    // per-wave gain (O-proj / FFN-down at 14B: 6 pair waves vs 5 single waves)
+    const long pairs = std::max(1L, sms / 2), tiles2 = ((a->m + 255) / 256) * (a->n / 256);
+    const long waves2 = (tiles2 + pairs - 1) / pairs, waves1 = (tiles_m * (a->n / 256) + sms - 1) / sms;
+    if (g_gemm2 && a->m >= 256 && (g_gemm2_all || waves2 * 23 < waves1 * 25)) return launch_gemm_tc2<256>(a, p, st);
     return launch_gemm_tc<256>(a, p, st);
+  }
   if (a->n % 128 == 0) return launch_gemm_tc<128>(a, p, st);
   if (a->n % 64 == 0) return launch_gemm_tc<64>(a, p, st);
   return fail(LP_EUNSUPPORTED, "gemm_tc: n must be a multiple of 64");
