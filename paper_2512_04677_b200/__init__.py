@@ -9,9 +9,12 @@ Keeps the reference ``livepipe`` model/pipeline API names for this path
 
 import os as _os
 
-# Stage links spin on the device; with lazy module loading a first-time kernel
-# launch can wait on a spinning waiter.  Must be set before CUDA initialises.
-_os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+# CUDA lazy module loading stays on (eager loading of every torch/cuBLAS/cuDNN
+# module costs minutes on a cold box).  Stage links spin on the device, and a
+# kernel loaded for the first time while a waiter spins could stall, so
+# liblivepipe_b200 loads all of its own kernels in lp_init and the TPP
+# runners warm the few torch kernels they launch (runtime.prewarm_torch)
+# before any link kernel is in flight.
 
 from .denoiser import (B200Denoiser, BlockCond, DenoiseOutput, KvEntry, TimestepForcingError,
                        check_view)

@@ -39,7 +39,7 @@ from .latent import Conditions, LatentBlock, TimestepSchedule, ToyVideoCodec, fl
 from .metrics import MetricsBundle, TimelineEvent, drift_metric, metrics_from_timeline
 from .model import DenoiserWeights, DeviceWeights, ModelProfile, build_weights, toy_profile
 from .numerics import F32, Prng
-from .runtime import Forward, KvArena, h2d, wait_event
+from .runtime import Forward, KvArena, h2d, prewarm_torch, wait_event
 
 THREADS_ENV = "LIVE_PIPE_THREADS"
 ORACLE_TARGET_STREAM = 1 << 46
@@ -497,6 +497,8 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
     devs = stage_devices(cfg)
     last_dev = devs[-1]
     nbytes = cfg.frames_per_block * prof.latent_dim * 4
+    for d in sorted(set(devs)):
+        prewarm_torch(f"cuda:{d}")
     abort = torch.zeros(4, dtype=torch.int32, device=f"cuda:{last_dev}")
     streams = [torch.cuda.Stream(d) for d in devs]
     stages = [Stage(cfg, rt, T - k + 1, devs[k - 1], streams[k - 1]) for k in range(1, T + 1)]

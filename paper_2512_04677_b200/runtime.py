@@ -45,6 +45,22 @@ def wait_event(ev) -> None:
         time.sleep(2e-5)
 
 
+def prewarm_torch(device) -> None:
+    """Load the torch kernels the stage runners launch while link kernels may
+    be spinning (fill / zeros / copies), so lazy module loading never happens
+    concurrently with a device-side wait."""
+    with torch.cuda.device(device):
+        a = torch.zeros(4, dtype=torch.int32, device=device)
+        a.fill_(1)
+        f = torch.zeros(8, dtype=torch.float32, device=device)
+        f.fill_(0.5)
+        f.copy_(torch.ones(8, device=device))
+        b = torch.empty(8, dtype=torch.bfloat16, device=device)
+        b.copy_(f)
+        f.copy_(b)
+        torch.cuda.synchronize(device)
+
+
 def h2d(dst: torch.Tensor, src_host, stream) -> torch.Event:
     """Asynchronous host->device copy through a fresh pinned staging tensor;
     returns the completion event (the staging tensor is kept alive by it)."""

@@ -54,6 +54,7 @@ from .engine import (EngineConfig, EngineConfigError, PipelineInvariantError, Ro
 from .kvcache import SinkSlot, receive_sink
 from .latent import LatentBlock
 from .metrics import TimelineEvent
+from .runtime import prewarm_torch
 from .numerics import F32
 
 # ---------------------------------------------------------------------------
@@ -481,6 +482,7 @@ class DistTPP:
         cfg = self.cfg
         dev = self.device
         nbytes = int(np.prod(self.backend.shape)) * 4
+        prewarm_torch(f"cuda:{dev}")
         self.abort = torch.zeros(4, dtype=torch.int32, device=f"cuda:{dev}")
         torch.cuda.synchronize(dev)
         self.link_in = None
