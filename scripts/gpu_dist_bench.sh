@@ -4,7 +4,7 @@
 OUT=gpurun_out/${1:-dist}
 mkdir -p $OUT
 python -c "import torch; torch.zeros(1).cuda()" > /dev/null 2>&1
-for n in 2 4; do
+for n in 2 4 8; do
   timeout 500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29512 \
     bench.py --gpus $n --steps 3 --warmup 3 --config 1.3b --dist-backend gloo --no-probe > $OUT/bench_n$n.json 2> $OUT/bench_n$n.err
   echo "n=$n rc=$?" >> $OUT/summary.txt
