@@ -67,11 +67,12 @@ def test_rollout_matches_reference(name):
     assert res.nfe == META[name]["nfe"]
 
 
-@pytest.mark.parametrize("name", ["c1", "c1_sigma", "c1_L1"])
-def test_tpp_bitwise_equals_sequential(name):
+@pytest.mark.parametrize("name,capacity", [("c1", 1), ("c1_sigma", 1), ("c1_L1", 1), ("c1", 2)])
+def test_tpp_bitwise_equals_sequential(name, capacity):
+    # threaded TPP (one stream per stage, device links of `capacity` slots)
     kw = META[name]["kw"]
     seq = lp.run_sequential(lp.EngineConfig(mode="sequential", **kw))
-    tpp = lp.run_tpp(lp.EngineConfig(mode="tpp", **kw))
+    tpp = lp.run_tpp(lp.EngineConfig(mode="tpp", link_capacity=capacity, **kw))
     assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(seq.blocks, tpp.blocks))
     assert seq.frames.tobytes() == tpp.frames.tobytes()
     assert tpp.nfe == seq.nfe
