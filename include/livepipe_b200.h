@@ -264,6 +264,22 @@ LP_API int lp_randn(float* out, int64_t n, uint64_t seed, uint64_t stream_id, fl
 LP_API int lp_randn_bf16(void* out, int64_t n, uint64_t seed, uint64_t stream_id, float scale,
                   void* stream);
 
+/* ---------------------------------------------------------------- codec
+ * The decode stage, run on the decode GPU.  The toy
+ * profile's ToyVideoCodec (latent.py:150-193) is a dense matvec per latent
+ * frame in the pinned matmul order and goes through lp_gemm (LP_F32).
+ * Patched (wan-shaped) profiles use a per-location patch codec standing in
+ * for the video VAE: latent (frames, C, H, W) fp32 -> pixels
+ * (frames*r, pc, H*s, W*s) fp32, pix[f*r+u][ch][h*s+dy][w*s+dx] =
+ * sum_c maps[u][(ch*s+dy)*s+dx][c] * x[f][c][h][w]; encode applies
+ * enc (C, pc*s*s) = pinv(maps[0]) to the s x s patches of one pixel frame
+ * (the AAS sink round trip, kvcache.py:93-109).  Pinned ascending order,
+ * no FMA contraction: bitwise equal to the NumPy restatement.  C <= 32.    */
+LP_API int lp_codec_patch_decode(const float* x, int frames, int C, int H, int W, const float* maps,
+                    int r, int pc, int s, float* out, void* stream);
+LP_API int lp_codec_patch_encode(const float* frame, int C, int H, int W, const float* enc, int pc,
+                    int s, float* out, void* stream);
+
 /* ---------------------------------------------------------------- TPP links
  * replace _Link.send/recv (engine.py:342-388) and the one-shot sink fan-out
  * (:417, :477-478).  A link is a ring of `capacity` payload slots plus

@@ -562,6 +562,45 @@ class Codec:
         ])
 
 
+class PatchCodec:
+    """Builder-defined stand-in for the video VAE on patched profiles (no
+    reference counterpart): the Codec contract above
+    (latent.py:150-193 -- r maps N(0,1)/sqrt(C) from the codec stream, encoder
+    = float64 pinv of map 0) applied per latent location.  Latent frame
+    (C, H, W); pixel frame (pc, H*s, W*s); map rows q = (ch*s + dy)*s + dx.
+    Sums are pinned (ascending c for decode, ascending q for encode)."""
+
+    def __init__(self, seed, channels, height, width, pixel_channels=3, scale=8, upsample=4):
+        g = philox(seed, STREAM_CODEC)
+        sc = F32(1.0 / np.sqrt(channels))
+        q = pixel_channels * scale * scale
+        self.C, self.H, self.W, self.pc, self.s, self.r = channels, height, width, pixel_channels, scale, upsample
+        self.maps = np.stack([g.standard_normal((q, channels), dtype=F32) * sc for _ in range(upsample)])
+        self.enc = np.linalg.pinv(self.maps[0].astype(np.float64)).astype(F32)
+
+    def decode(self, block_values):
+        C, H, W, pc, s, r = self.C, self.H, self.W, self.pc, self.s, self.r
+        lat = np.asarray(block_values, F32).reshape(-1, C, H * W)
+        out = []
+        for f in range(lat.shape[0]):
+            for u in range(r):
+                acc = np.zeros((pc * s * s, H * W), F32)
+                for c in range(C):
+                    acc += np.multiply.outer(self.maps[u][:, c], lat[f, c])
+                # (ch, dy, dx, h, w) -> (ch, h, dy, w, dx)
+                img = acc.reshape(pc, s, s, H, W).transpose(0, 3, 1, 4, 2).reshape(-1)
+                out.append(img)
+        return np.stack(out)
+
+    def encode(self, frame):
+        C, H, W, pc, s = self.C, self.H, self.W, self.pc, self.s
+        pix = np.asarray(frame, F32).reshape(pc, H, s, W, s).transpose(0, 2, 4, 1, 3).reshape(pc * s * s, H * W)
+        acc = np.zeros((C, H * W), F32)
+        for q in range(pc * s * s):
+            acc += np.multiply.outer(self.enc[:, q], pix[q])
+        return acc.reshape(-1)
+
+
 # ---------------------------------------------------------------------------
 # rollouts (engine.py:204-285, Algorithm 3 / 4)
 # ---------------------------------------------------------------------------
@@ -605,7 +644,8 @@ def run_sequential(cfg: RolloutCfg, weights: Weights | None = None, mm=mm_pinned
     p = cfg.profile
     w = weights if weights is not None else build_weights(cfg.weight_seed, p)
     audio, prompt, ref = conditions(cfg)
-    cd = Codec(cfg.weight_seed, p.latent_dim, cfg.pixel_dim, cfg.upsample) if codec else None
+    cd = codec if hasattr(codec, "decode") else (Codec(cfg.weight_seed, p.latent_dim, cfg.pixel_dim, cfg.upsample)
+                                                    if codec else None)
     dt = -1.0 / cfg.steps
     caches = {j: [] for j in range(1, cfg.steps + 1)}
     sink = ref.copy()
@@ -639,7 +679,8 @@ def run_clean_kv(cfg: RolloutCfg, weights: Weights | None = None, mm=mm_pinned, 
     p = cfg.profile
     w = weights if weights is not None else build_weights(cfg.weight_seed, p)
     audio, prompt, ref = conditions(cfg)
-    cd = Codec(cfg.weight_seed, p.latent_dim, cfg.pixel_dim, cfg.upsample) if codec else None
+    cd = codec if hasattr(codec, "decode") else (Codec(cfg.weight_seed, p.latent_dim, cfg.pixel_dim, cfg.upsample)
+                                                    if codec else None)
     dt = -1.0 / cfg.steps
     unified = []
     sink = ref.copy()

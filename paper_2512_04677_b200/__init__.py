@@ -23,8 +23,9 @@ from .engine import (EngineConfig, EngineConfigError, PipelineInvariantError, Ro
                      StreamingPipeline)
 from .kvcache import (RollingKvCache, SinkLockedError, SinkSlot, aas_update, cache_push, corrupt_history,
                       corruption_prng, receive_sink, rolling_rope_index)
-from .latent import (Conditions, LatentBlock, TimestepSchedule, ToyVideoCodec, flow_step, interpolate,
-                     synthetic_conditions, true_velocity)
+from .latent import (Conditions, LatentBlock, PatchVideoCodec, TimestepSchedule, ToyVideoCodec, flow_step,
+                     interpolate, synthetic_conditions, true_velocity)
+from .codec import DeviceCodec
 from .metrics import (MetricsBundle, TimelineEvent, compute_fps, compute_ttff, drift_metric,
                       metrics_from_timeline, stage_utilization)
 from .model import (WAN_14B, WAN_1_3B, DenoiserWeights, DeviceWeights, LayerWeights, ModelProfile,

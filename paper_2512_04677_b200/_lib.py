@@ -88,6 +88,9 @@ _SIGS = {
     "lp_patchify": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
     "lp_unpatchify_euler": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp],
                             C.c_int),
+    "lp_codec_patch_decode": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, vp],
+                              C.c_int),
+    "lp_codec_patch_encode": ([vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp], C.c_int),
     "lp_history_noise": ([vp, C.c_int, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
     "lp_randn": ([vp, i64, u64, u64, C.c_float, vp], C.c_int),
     "lp_randn_bf16": ([vp, i64, u64, u64, C.c_float, vp], C.c_int),

@@ -54,6 +54,9 @@ int preload_f32();
 int preload_rows();
 int preload_gemm_tc();
 int preload_attn_tc();
+int preload_codec();
+int codec_patch_decode(const float*, int, int, int, int, const float*, int, int, int, float*, cudaStream_t);
+int codec_patch_encode(const float*, int, int, int, const float*, int, int, float*, cudaStream_t);
 
 }  // namespace lp
 
@@ -83,7 +86,7 @@ int lp_init(int device) {
   // loaded kernel launched while a waiter spins can stall in the loader.
   int rc;
   if ((rc = preload_links()) || (rc = preload_f32()) || (rc = preload_rows()) || (rc = preload_gemm_tc()) ||
-      (rc = preload_attn_tc()))
+      (rc = preload_attn_tc()) || (rc = preload_codec()))
     return rc;
   return tma_init();
 }
@@ -202,6 +205,18 @@ int lp_link_recv(const void* src_slot, void* dst, int64_t bytes, volatile const 
                  int32_t* status_out, void* stream) {
   return link_recv(src_slot, dst, bytes, ready_flag, free_flag, seq, abort_word, timeout_ns, status_out,
                    S(stream));
+}
+
+int lp_codec_patch_decode(const float* x, int frames, int C, int H, int W, const float* maps, int r, int pc, int s,
+                          float* out, void* stream) {
+  LP_CHECK_ARG(x && maps && out, "lp_codec_patch_decode: null argument");
+  return codec_patch_decode(x, frames, C, H, W, maps, r, pc, s, out, S(stream));
+}
+
+int lp_codec_patch_encode(const float* frame, int C, int H, int W, const float* enc, int pc, int s, float* out,
+                          void* stream) {
+  LP_CHECK_ARG(frame && enc && out, "lp_codec_patch_encode: null argument");
+  return codec_patch_encode(frame, C, H, W, enc, pc, s, out, S(stream));
 }
 
 int lp_signal(volatile uint32_t* flag, uint32_t value, void* stream) { return signal(flag, value, S(stream)); }

@@ -26,7 +26,7 @@ import os
 import queue
 import threading
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -35,7 +35,9 @@ from . import _lib as L
 from .denoiser import B200Denoiser, BlockCond
 from .kvcache import RingIndex, RollingKvCache, SinkSlot, aas_update, corrupt_history, corruption_prng, receive_sink, \
     rolling_rope_index
-from .latent import Conditions, LatentBlock, TimestepSchedule, ToyVideoCodec, flow_step, synthetic_conditions
+from .codec import DeviceCodec
+from .latent import (Conditions, LatentBlock, PatchVideoCodec, TimestepSchedule, ToyVideoCodec, flow_step,
+                     synthetic_conditions)
 from .metrics import MetricsBundle, TimelineEvent, drift_metric, metrics_from_timeline
 from .model import DenoiserWeights, DeviceWeights, ModelProfile, build_weights, toy_profile
 from .numerics import F32, Prng
@@ -92,6 +94,12 @@ class EngineConfig:
     use_graphs: bool = True
     device_inputs: bool = False  # perf runs: weights / noise from the device RNG
     link_timeout_s: float = 60.0
+    # patched profiles: decode through the per-location patch codec (the VAE
+    # stand-in, latent.PatchVideoCodec) with pixel_channels x pixel_scale^2
+    # pixels per latent location; off = no frames, sink = block 0's frame 0
+    patch_codec: bool = False
+    pixel_channels: int = 3
+    pixel_scale: int = 8
 
     def __post_init__(self):
         if self.mode not in MODES:
@@ -99,7 +107,7 @@ class EngineConfig:
         if self.denoiser_kind not in DENOISER_KINDS:
             raise EngineConfigError(f"denoiser must be one of {DENOISER_KINDS}")
         for name in ("steps", "cache_capacity", "frames_per_block", "blocks", "upsample", "sink_delta",
-                     "n_layers", "n_heads", "head_dim", "link_capacity"):
+                     "n_layers", "n_heads", "head_dim", "link_capacity", "pixel_channels", "pixel_scale"):
             if getattr(self, name) < 1:
                 raise EngineConfigError(f"{name} must be >= 1")
         if self.history_sigma < 0.0:
@@ -161,8 +169,9 @@ class Runtime:
     schedule: TimestepSchedule
     weights: DenoiserWeights | None
     device_weights: dict  # device index -> DeviceWeights
-    codec: ToyVideoCodec | None
+    codec: ToyVideoCodec | PatchVideoCodec | None
     conditions: Conditions
+    device_codecs: dict = field(default_factory=dict)  # device index -> codec.DeviceCodec
 
 
 def build_runtime(cfg: EngineConfig) -> Runtime:
@@ -181,6 +190,9 @@ def build_runtime(cfg: EngineConfig) -> Runtime:
     codec = None
     if not prof.patched:
         codec = ToyVideoCodec(cfg.weight_seed, prof.latent_dim, cfg.pixel_dim, cfg.upsample)
+    elif cfg.patch_codec:
+        codec = PatchVideoCodec(cfg.weight_seed, prof.channels, prof.height, prof.width, cfg.pixel_channels,
+                                cfg.pixel_scale, cfg.upsample)
     conds = synthetic_conditions(cfg.noise_seed, cfg.blocks, prof.audio_dim, prof.prompt_dim, prof.latent_dim)
     return Runtime(schedule, w, dws, codec, conds)
 
@@ -347,7 +359,7 @@ def _finish(cfg, rt, blocks, chunks, nfe, sink_content, timeline) -> RolloutResu
     frames = np.concatenate(chunks) if chunks else None
     metrics = None
     if timeline:
-        drift = drift_metric(frames, rt.codec.decode_frame(sink_content)[0]) if (frames is not None) else None
+        drift = drift_metric(frames, _dcodec(rt).decode_frame(sink_content)[0]) if (frames is not None) else None
         try:
             metrics = metrics_from_timeline(timeline, cfg.total_frames, cfg.arrival_offset, nfe, drift)
         except ValueError:
@@ -355,13 +367,27 @@ def _finish(cfg, rt, blocks, chunks, nfe, sink_content, timeline) -> RolloutResu
     return RolloutResult(tuple(blocks), frames, nfe, timeline, metrics)
 
 
-def _decode(rt: Runtime, x: LatentBlock):
-    return rt.codec.decode(x) if rt.codec is not None else None
+def _dcodec(rt: Runtime, dev: int | None = None) -> DeviceCodec | None:
+    """The decode stage's codec on device `dev`."""
+    if rt.codec is None:
+        return None
+    if dev is None:
+        dev = min(rt.device_weights) if rt.device_weights else 0
+    dc = rt.device_codecs.get(dev)
+    if dc is None:
+        dc = rt.device_codecs.setdefault(dev, DeviceCodec(rt.codec, dev))
+    return dc
 
 
-def _aas(rt: Runtime, sink: SinkSlot, x: LatentBlock) -> None:
+def _decode(rt: Runtime, x: LatentBlock, dev: int | None = None):
+    """decode(block) on the GPU (engine.py:279 / :460 -> latent.py:189-193)."""
+    dc = _dcodec(rt, dev)
+    return dc.decode(x) if dc is not None else None
+
+
+def _aas(rt: Runtime, sink: SinkSlot, x: LatentBlock, dev: int | None = None) -> None:
     if rt.codec is not None:
-        aas_update(sink, x, rt.codec)
+        aas_update(sink, x, _dcodec(rt, dev))
     else:
         # patched profiles: the decode stage is "next" (SURVEY.md 8f); the
         # sink takes block 0's first latent frame (the round trip's fixed point)
@@ -414,11 +440,11 @@ def run_sequential(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResul
             xb = LatentBlock(out.numpy(), i)
             blocks.append(xb)
             ds = time.perf_counter() - t0_host
-            fr = _decode(rt, xb)
+            fr = _decode(rt, xb, dev)
             if fr is not None:
                 chunks.append(fr)
             if i == 0:
-                _aas(rt, sink, xb)
+                _aas(rt, sink, xb, dev)
                 for st in stages.values():
                     st.set_sink(sink.content)
             dec_t.append((i, ds, time.perf_counter() - t0_host))
@@ -577,9 +603,9 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
                 ds = time.perf_counter() - t0_host
                 xb = LatentBlock(host.numpy(), i)
                 out_blocks[i] = xb
-                out_chunks[i] = _decode(rt, xb)
+                out_chunks[i] = _decode(rt, xb, dev)
                 if i == 0:
-                    _aas(rt, decoder_sink, xb)
+                    _aas(rt, decoder_sink, xb, dev)
                     for feed in sink_feeds:
                         feed.put(decoder_sink.content)
                 dec_t.append((i, ds, time.perf_counter() - t0_host))
@@ -636,11 +662,11 @@ def run_clean_kv(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
         nfe += 1
         unified.push(entry)
         blocks.append(x)
-        fr = _decode(rt, x)
+        fr = _decode(rt, x, cfg.devices[0])
         if fr is not None:
             chunks.append(fr)
         if i == 0:
-            _aas(rt, sink, x)
+            _aas(rt, sink, x, cfg.devices[0])
     return _finish(cfg, rt, blocks, chunks, nfe, sink.content, ())
 
 
@@ -705,6 +731,6 @@ class StreamingPipeline:
     def aas(self, block0: torch.Tensor) -> None:
         """One-shot sink swap after block 0 (kvcache.py:93-109)."""
         xb = LatentBlock(block0.detach().float().cpu().numpy().reshape(self.cfg.frames_per_block, -1), 0)
-        _aas(self.rt, self.sink, xb)
+        _aas(self.rt, self.sink, xb, self.dev)
         for st in self.stages.values():
             st.set_sink(self.sink.content)

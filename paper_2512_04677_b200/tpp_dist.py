@@ -550,7 +550,7 @@ class DistTPP:
 
     def _aas_last(self, xb: LatentBlock) -> None:
         if self.rt is not None:
-            _aas(self.rt, self.sink, xb)
+            _aas(self.rt, self.sink, xb, self.device)
         else:
             self.backend.aas(self.sink, xb)
         self._sink_broadcast(self.sink.content)
@@ -602,7 +602,7 @@ class DistTPP:
                 xb = self.step(i)
                 if xb is not None:
                     blocks.append(xb)
-                    fr = _decode(self.rt, xb) if self.rt is not None else self.backend.decode(xb)
+                    fr = _decode(self.rt, xb, self.device) if self.rt is not None else self.backend.decode(xb)
                     if fr is not None:
                         chunks.append(fr)
                     dec_t.append(TimelineEvent(len(self.roles[0].ranks) + 1, i, s, time.perf_counter() - t0,
