@@ -24,37 +24,23 @@ namespace lp {
 constexpr int CODEC_MAX_C = 32;
 constexpr int CODEC_THREADS = 128;
 
-__device__ __forceinline__ uint64_t pk2(float a, float b) {
-  return (uint64_t)__float_as_uint(a) | ((uint64_t)__float_as_uint(b) << 32);
-}
-__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {  // two separately rounded products
-  uint64_t r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-
-// grid (ceil(W / 128), H, frames * r); one thread per latent location.  The
+// grid (ceil(W / 128), H * pc, frames * r); one thread per (latent location,
+// pixel channel): s x s outputs.  The
 // map is staged transposed (c-major) so that four adjacent dx outputs take
-// one 16-byte shared load per channel; products and sums are packed f32x2
-// (mul.rn / add.rn, never contracted into an FMA).
+// one 16-byte shared load per channel.
 template <int VEC, int NC>
 __global__ void __launch_bounds__(CODEC_THREADS, 4) codec_patch_decode_kernel(const float* __restrict__ x, int C, int H,
                                                                            int W, const float* __restrict__ maps,
                                                                            int r, int pc, int s,
                                                                            float* __restrict__ out) {
-  extern __shared__ __align__(16) float sm_map[];  // C x Q of map u
-  const int Q = pc * s * s;
+  extern __shared__ __align__(16) float sm_map[];  // C x (s*s): rows of map u for channel ch
+  const int SS = s * s;
   const int fu = blockIdx.z, u = fu % r, f = fu / r;
-  const int h = blockIdx.y, w = blockIdx.x * CODEC_THREADS + threadIdx.x;
-  const float* mu = maps + (int64_t)u * Q * C;
-  for (int e = threadIdx.x; e < Q * C; e += CODEC_THREADS) {
+  const int h = blockIdx.y / pc, ch = blockIdx.y - h * pc, w = blockIdx.x * CODEC_THREADS + threadIdx.x;
+  const float* mu = maps + ((int64_t)u * pc + ch) * SS * C;
+  for (int e = threadIdx.x; e < SS * C; e += CODEC_THREADS) {
     const int q = e / C, c = e - q * C;
-    sm_map[c * Q + q] = mu[e];
+    sm_map[c * SS + q] = mu[e];
   }
   __syncthreads();
   if (w >= W) return;
@@ -66,32 +52,34 @@ __global__ void __launch_bounds__(CODEC_THREADS, 4) codec_patch_decode_kernel(co
 
   const int64_t ow = (int64_t)W * s, oh = (int64_t)H * s;
   float* of = out + (int64_t)fu * pc * oh * ow;
-#pragma unroll 1
-  for (int ch = 0; ch < pc; ++ch) {
+  {
 #pragma unroll 1
     for (int dy = 0; dy < s; ++dy) {
       float* orow = of + ((int64_t)ch * oh + (int64_t)h * s + dy) * ow + (int64_t)w * s;
-      const int q0 = (ch * s + dy) * s;
+      const int q0 = dy * s;
 #pragma unroll 1
       for (int dx = 0; dx < s; dx += VEC) {
         if constexpr (VEC == 4) {
-          uint64_t a01 = 0, a23 = 0;  // +0.0f pairs, as np.zeros
+          // scalar mul.rn / add.rn: ptxas contracts the packed f32x2 forms
+          // (mul.rn.f32x2 + add.rn.f32x2 -> FFMA2, checked in the SASS),
+          // which would break the pinned rounding
+          float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
             if (c < C) {
-              const float4 m = *reinterpret_cast<const float4*>(sm_map + c * Q + q0 + dx);
-              const uint64_t xx = pk2(xr[c], xr[c]);
-              a01 = add2(a01, mul2(pk2(m.x, m.y), xx));
-              a23 = add2(a23, mul2(pk2(m.z, m.w), xx));
+              const float4 m = *reinterpret_cast<const float4*>(sm_map + c * SS + q0 + dx);
+              a0 = __fadd_rn(a0, __fmul_rn(m.x, xr[c]));
+              a1 = __fadd_rn(a1, __fmul_rn(m.y, xr[c]));
+              a2 = __fadd_rn(a2, __fmul_rn(m.z, xr[c]));
+              a3 = __fadd_rn(a3, __fmul_rn(m.w, xr[c]));
             }
           }
-          *reinterpret_cast<uint4*>(orow + dx) =
-              make_uint4((uint32_t)a01, (uint32_t)(a01 >> 32), (uint32_t)a23, (uint32_t)(a23 >> 32));
+          *reinterpret_cast<float4*>(orow + dx) = make_float4(a0, a1, a2, a3);
         } else {
           float acc = 0.0f;
 #pragma unroll
           for (int c = 0; c < NC; ++c)
-            if (c < C) acc = __fadd_rn(acc, __fmul_rn(sm_map[c * Q + q0 + dx], xr[c]));
+            if (c < C) acc = __fadd_rn(acc, __fmul_rn(sm_map[c * SS + q0 + dx], xr[c]));
           orow[dx] = acc;
         }
       }
@@ -141,8 +129,9 @@ int codec_patch_decode(const float* x, int frames, int C, int H, int W, const fl
   if (rc) return rc;
   LP_CHECK_ARG(frames >= 1 && r >= 1 && frames * r <= 65535, "codec: bad frame count");
   LP_CHECK_ARG(H <= 65535, "codec: H too large");
-  const size_t smem = (size_t)pc * s * s * C * sizeof(float);
-  dim3 grid((W + CODEC_THREADS - 1) / CODEC_THREADS, H, frames * r);
+  const size_t smem = (size_t)s * s * C * sizeof(float);
+  LP_CHECK_ARG((int64_t)H * pc <= 65535, "codec: H * pixel channels too large");
+  dim3 grid((W + CODEC_THREADS - 1) / CODEC_THREADS, H * pc, frames * r);
   auto launch = [&](auto kern) -> int {
     if (smem > 48 * 1024)
       LP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
