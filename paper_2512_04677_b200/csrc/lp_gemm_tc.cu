@@ -520,6 +520,7 @@ int preload_gemm_tc() {
 
 static bool g_gemm2 = getenv("LP_NO_GEMM2") == nullptr;      // LP_NO_GEMM2=1 forces 1-CTA tiles
 static bool g_gemm2_all = getenv("LP_GEMM2_ALL") != nullptr;  // LP_GEMM2_ALL=1: pairs whenever N % 256 == 0
+static bool g_gemm2_qkv = getenv("LP_NO_GEMM2_QKV") == nullptr;  // LP_NO_GEMM2_QKV=1: 1-CTA QKV tiles
 
 int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
   LP_CHECK_ARG(num_sms() > 0, "lp_init() must be called before the tcgen05 GEMM");
@@ -549,8 +550,16 @@ int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
     p.qkv = *a->qkv;
     LP_CHECK_ARG(a->n == 3 * p.qkv.d && p.qkv.head_dim % 32 == 0, "gemm_tc: QKV shape");
     LP_CHECK_ARG(p.qkv.d % 256 == 0 || p.qkv.d % 128 == 0, "gemm_tc: QKV needs d % 128 == 0");
-    if (p.qkv.d % 256 == 0 && p.qkv.head_dim <= 256 && 256 % p.qkv.head_dim == 0)
+    if (p.qkv.d % 256 == 0 && p.qkv.head_dim <= 256 && 256 % p.qkv.head_dim == 0) {
+      // cluster pairs under the same wave rule as the plain GEMMs below (each
+      // CTA of a pair runs the per-row epilogue on its own 128 rows)
+      const long sms = std::max(1, num_sms()), pairs = std::max(1L, sms / 2);
+      const long waves2 = (((a->m + 255) / 256) * (a->n / 256) + pairs - 1) / pairs;
+      const long waves1 = (((a->m + GBM - 1) / GBM) * (a->n / 256) + sms - 1) / sms;
+      if (g_gemm2 && g_gemm2_qkv && a->m >= 256 && (g_gemm2_all || waves2 * 23 < waves1 * 25))
+        return launch_gemm_tc2<256>(a, p, st);
       return launch_gemm_tc<256>(a, p, st);
+    }
     LP_CHECK_ARG(128 % p.qkv.head_dim == 0, "gemm_tc: head_dim must divide the tile");
     return launch_gemm_tc<128>(a, p, st);
   }

@@ -81,11 +81,13 @@ def test_gated_residual_epilogue():
     assert rel_l2(h.cpu(), ref.cpu()) < 1e-5
 
 
-@pytest.mark.parametrize("qk_norm,spatial", [(False, False), (True, True)])
-def test_qkv_epilogue(qk_norm, spatial):
-    n_heads, hd = 4, 128
+@pytest.mark.parametrize("qk_norm,spatial,n_heads,frames", [(False, False, 4, 0), (True, True, 4, 3),
+                                                             (True, True, 8, 5)])
+def test_qkv_epilogue(qk_norm, spatial, n_heads, frames):
+    # m >= 256 takes the cluster-pair kernel (390 / 650 tokens: ragged last pair tile)
+    hd = 128
     d = n_heads * hd
-    n_tok = 390 if spatial else 200
+    n_tok = 130 * frames if spatial else 200
     a, w = _ab(n_tok, d, 3 * d, 3)
     if spatial:
         third = hd // 6
