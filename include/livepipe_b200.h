@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LP_ABI_VERSION 1
+#define LP_ABI_VERSION 2
 
 /* status codes */
 #define LP_OK 0
@@ -152,8 +152,19 @@ typedef struct lp_gemm_args {
   const float* gate;      /* [n] or NULL (RESID only)                       */
   const lp_qkv_epi* qkv;  /* host pointer, LP_EPI_QKV only                  */
   const lp_euler_epi* euler; /* host pointer, LP_EPI_EULER only             */
+  void* fork;             /* lp_fork_create handle or NULL: lets a bf16 GEMM
+                             whose M is not a multiple of 256 run cluster-pair
+                             tiles on the whole 256-row blocks and the ragged
+                             rows as single-CTA tiles on the handle's side
+                             stream, concurrently (fork/join events on
+                             `stream`; graph-capture safe)                   */
 } lp_gemm_args;
 LP_API int lp_gemm(const lp_gemm_args* args, void* stream);
+
+/* Side stream + fork/join events for lp_gemm_args.fork; create outside any
+   stream capture, one per concurrently used stream.                        */
+LP_API int lp_fork_create(void** out);
+LP_API int lp_fork_destroy(void* fork);
 
 /* ---------------------------------------------------------------- attention
  * replaces the per-head loop of denoise_block (denoiser.py:246-264) and

@@ -17,6 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LIVEPIPE_LIB") or os.path.join(HERE, "liblivepipe_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "livepipe_b200.h")
 
+ABI_VERSION = 2  # LP_ABI_VERSION in include/livepipe_b200.h
 LP_OK, LP_EINVAL, LP_ECUDA, LP_EUNSUPPORTED, LP_ETIMEOUT, LP_EABORT = range(6)
 LP_F32, LP_BF16 = 0, 1
 EPI_STORE, EPI_RELU, EPI_GELU, EPI_RESID, EPI_QKV, EPI_EULER = range(6)
@@ -58,7 +59,8 @@ class EulerEpi(C.Structure):
 class GemmArgs(C.Structure):
     _fields_ = [("in_dtype", i32), ("out_dtype", i32), ("epilogue", i32), ("m", i32), ("n", i32),
                 ("k", i32), ("lda", i64), ("ldw", i64), ("ldc", i64), ("a", vp), ("w", vp), ("c", vp),
-                ("bias", vp), ("gate", vp), ("qkv", C.POINTER(QkvEpi)), ("euler", C.POINTER(EulerEpi))]
+                ("bias", vp), ("gate", vp), ("qkv", C.POINTER(QkvEpi)), ("euler", C.POINTER(EulerEpi)),
+                ("fork", vp)]
 
 
 class AttnArgs(C.Structure):
@@ -88,6 +90,8 @@ _SIGS = {
     "lp_patchify": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
     "lp_unpatchify_euler": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp],
                             C.c_int),
+    "lp_fork_create": ([C.POINTER(vp)], C.c_int),
+    "lp_fork_destroy": ([vp], C.c_int),
     "lp_codec_patch_decode": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, vp],
                               C.c_int),
     "lp_codec_patch_encode": ([vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp], C.c_int),
@@ -137,7 +141,7 @@ def load() -> C.CDLL:
                 fn = getattr(lib, name)
                 fn.argtypes = args
                 fn.restype = res
-            if lib.lp_abi_version() != 1:
+            if lib.lp_abi_version() != ABI_VERSION:
                 raise ImportError("liblivepipe_b200 ABI version mismatch")
             _lib = lib
     return _lib
@@ -149,6 +153,13 @@ def call(name: str, *args) -> None:
     if rc != LP_OK:
         msg = lib.lp_last_error().decode(errors="replace")
         raise LivepipeError(name, rc, msg)
+
+
+def fork_create() -> int:
+    """lp_fork_create: side stream + events for lp_gemm_args.fork."""
+    h = C.c_void_p()
+    call("lp_fork_create", C.byref(h))
+    return h.value
 
 
 def init_device(device: int) -> None:

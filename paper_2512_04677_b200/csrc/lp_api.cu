@@ -55,6 +55,8 @@ int preload_rows();
 int preload_gemm_tc();
 int preload_attn_tc();
 int preload_codec();
+int fork_create(void**);
+int fork_destroy(void*);
 int codec_patch_decode(const float*, int, int, int, int, const float*, int, int, int, float*, cudaStream_t);
 int codec_patch_encode(const float*, int, int, int, const float*, int, int, float*, cudaStream_t);
 
@@ -206,6 +208,10 @@ int lp_link_recv(const void* src_slot, void* dst, int64_t bytes, volatile const 
   return link_recv(src_slot, dst, bytes, ready_flag, free_flag, seq, abort_word, timeout_ns, status_out,
                    S(stream));
 }
+
+int lp_fork_create(void** out) { return fork_create(out); }
+
+int lp_fork_destroy(void* fork) { return fork_destroy(fork); }
 
 int lp_codec_patch_decode(const float* x, int frames, int C, int H, int W, const float* maps, int r, int pc, int s,
                           float* out, void* stream) {

@@ -29,6 +29,7 @@ constexpr int G_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2
 
 struct GemmParams {
   int m, n, k;
+  int m_begin, m_end;  // tiles cover rows [m_begin, m_end); rows >= m are discarded
   int epilogue, out_dtype;
   void* c;
   int64_t ldc;
@@ -36,6 +37,11 @@ struct GemmParams {
   const float* gate;
   lp_qkv_epi qkv;
   lp_euler_epi euler;
+};
+
+struct ForkCtx {
+  cudaStream_t side;
+  cudaEvent_t fork, join;
 };
 
 template <int BN>
@@ -224,7 +230,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int tiles_m = (p.m + GBM - 1) / GBM, tiles_n = p.n / BN;
+  const int tiles_m = (p.m_end - p.m_begin + GBM - 1) / GBM, tiles_n = p.n / BN;
   const int num_tiles = tiles_m * tiles_n;
   const int num_kb = p.k / GBK;
 
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       uint32_t phase = 0;
       const uint64_t pol_a = l2_policy_evict_last();
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile % tiles_m) * GBM, n0 = (tile / tiles_m) * BN;
+        const int m0 = p.m_begin + (tile % tiles_m) * GBM, n0 = (tile / tiles_m) * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * SM::STAGE_BYTES;
@@ -310,7 +316,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int acc = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
-      const int m0 = (tile % tiles_m) * GBM, n0 = (tile / tiles_m) * BN;
+      const int m0 = p.m_begin + (tile % tiles_m) * GBM, n0 = (tile / tiles_m) * BN;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int row = m0 + quarter * 32 + lane;
@@ -364,7 +370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_ctarank();
-  const int tiles_m = (p.m + 2 * GBM - 1) / (2 * GBM), tiles_n = p.n / BN;
+  const int tiles_m = (p.m_end - p.m_begin + 2 * GBM - 1) / (2 * GBM), tiles_n = p.n / BN;
   const int num_tiles = tiles_m * tiles_n;
   const int num_kb = p.k / GBK;
   const int cid = blockIdx.x >> 1, nclu = gridDim.x >> 1;
@@ -396,7 +402,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
       uint32_t phase = 0;
       const uint64_t pol = l2_policy_evict_last();
       for (int tile = cid; tile < num_tiles; tile += nclu) {
-        int m0 = (tile % tiles_m) * 2 * GBM + rank * GBM;
+        int m0 = p.m_begin + (tile % tiles_m) * 2 * GBM + rank * GBM;
         if (m0 >= p.m) m0 = p.m > GBM ? p.m - GBM : 0;  // wholly past M: load valid rows, results discarded
         const int n0 = (tile / tiles_m) * BN + rank * (BN / 2);
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -455,7 +461,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
     for (int tile = cid; tile < num_tiles; tile += nclu, ++local) {
       const int acc = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
-      const int m0 = (tile % tiles_m) * 2 * GBM + rank * GBM, n0 = (tile / tiles_m) * BN;
+      const int m0 = p.m_begin + (tile % tiles_m) * 2 * GBM + rank * GBM, n0 = (tile / tiles_m) * BN;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int row = m0 + quarter * 32 + lane;
@@ -484,7 +490,7 @@ static int launch_gemm_tc2(const lp_gemm_args* a, const GemmParams& p, cudaStrea
   if (rc) return rc;
   rc = make_tmap_bf16_2d(&tb, a->w, (uint64_t)a->n, (uint64_t)a->k, (uint64_t)a->ldw, BN / 2, GBK);
   if (rc) return rc;
-  const int tiles = ((a->m + 2 * GBM - 1) / (2 * GBM)) * (a->n / BN);
+  const int tiles = ((p.m_end - p.m_begin + 2 * GBM - 1) / (2 * GBM)) * (a->n / BN);
   const int clusters = std::min(tiles, std::max(1, num_sms() / 2));
   const int smem = Gemm2Smem<BN>::TOTAL;
   auto kern = gemm_tc2_kernel<BN>;
@@ -500,13 +506,37 @@ static int launch_gemm_tc(const lp_gemm_args* a, const GemmParams& p, cudaStream
   if (rc) return rc;
   rc = make_tmap_bf16_2d(&tb, a->w, (uint64_t)a->n, (uint64_t)a->k, (uint64_t)a->ldw, BN, GBK);
   if (rc) return rc;
-  const int tiles = ((a->m + GBM - 1) / GBM) * (a->n / BN);
+  const int tiles = ((p.m_end - p.m_begin + GBM - 1) / GBM) * (a->n / BN);
   const int grid = std::min(tiles, std::max(1, num_sms()));
   const int smem = GemmSmem<BN>::TOTAL;
   auto kern = gemm_tc_kernel<BN>;
   LP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<grid, G_THREADS, smem, st>>>(ta, tb, p);
   return launch_status("gemm_tc");
+}
+
+int fork_create(void** out) {
+  LP_CHECK_ARG(out, "lp_fork_create: null argument");
+  ForkCtx* f = new ForkCtx();
+  cudaError_t e = cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->join, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    delete f;
+    return fail(LP_ECUDA, std::string("lp_fork_create: ") + cudaGetErrorString(e));
+  }
+  *out = f;
+  return LP_OK;
+}
+
+int fork_destroy(void* h) {
+  if (!h) return LP_OK;
+  ForkCtx* f = static_cast<ForkCtx*>(h);
+  cudaEventDestroy(f->fork);
+  cudaEventDestroy(f->join);
+  cudaStreamDestroy(f->side);
+  delete f;
+  return LP_OK;
 }
 
 int preload_gemm_tc() {
@@ -521,6 +551,44 @@ int preload_gemm_tc() {
 static bool g_gemm2 = getenv("LP_NO_GEMM2") == nullptr;      // LP_NO_GEMM2=1 forces 1-CTA tiles
 static bool g_gemm2_all = getenv("LP_GEMM2_ALL") != nullptr;  // LP_GEMM2_ALL=1: pairs whenever N % 256 == 0
 static bool g_gemm2_qkv = getenv("LP_NO_GEMM2_QKV") == nullptr;  // LP_NO_GEMM2_QKV=1: 1-CTA QKV tiles
+static bool g_split = getenv("LP_NO_PAIR_SPLIT") == nullptr;     // LP_NO_PAIR_SPLIT=1: no pair + tail split
+
+// Cluster pairs on the rows [0, m_pair) that whole 256-row pair tiles cover,
+// and the ragged last rows (m - m_pair < 256) as single-CTA tiles on the
+// fork context's side stream, concurrently: the pair kernel's last wave
+// leaves 2 * (pairs * waves - tiles) SMs idle, and the tail tiles run there.
+// At 14B (m = 4680) this turns O-proj / FFN-down from 5 single-CTA waves
+// into 5 pair waves (whose tiles read half of B per CTA) and QKV from 16 to
+// 15 pair waves.  Returns 1 when the split does not apply.
+// Wave costs in the comparison: a pair wave 100, a single-CTA wave 115 (the
+// 14B GEMMs run at 96 % vs 81-84 % of the tensor pipe: single-CTA tiles read
+// all of B per CTA and are L2-feed bound).  LP_PAIR_SPLIT_ALL forces the split
+// whenever the shape allows it (tests of small shapes).
+static int launch_pair_split(const lp_gemm_args* a, const GemmParams& p, cudaStream_t st, long waves_now,
+                             bool pair_now) {
+  if (!a->fork || !g_gemm2 || !g_split || a->n % 256 != 0) return 1;
+  const long sms = std::max(1, num_sms()), pairs = std::max(1L, sms / 2);
+  const long m_pair = (a->m / 256) * 256;
+  if (m_pair < 256 || m_pair == a->m) return 1;
+  const long tiles2 = (m_pair / 256) * (a->n / 256), waves2 = (tiles2 + pairs - 1) / pairs;
+  const long idle = 2 * (pairs * waves2 - tiles2), tail = ((a->m - m_pair + GBM - 1) / GBM) * (a->n / 256);
+  const long t_now = waves_now * (pair_now ? 100 : 115);
+  const long t_split = waves2 * 100 + (tail > idle ? 115 * ((tail - idle + sms - 1) / sms) : 0) + 2;
+  if (getenv("LP_PAIR_SPLIT_ALL") == nullptr && t_split >= t_now) return 1;
+  const ForkCtx* f = static_cast<const ForkCtx*>(a->fork);
+  GemmParams pp = p, pt = p;
+  pp.m_end = (int)m_pair;
+  pt.m_begin = (int)m_pair;
+  LP_CUDA_TRY(cudaEventRecord(f->fork, st));
+  LP_CUDA_TRY(cudaStreamWaitEvent(f->side, f->fork, 0));
+  int rc = launch_gemm_tc2<256>(a, pp, st);  // launched first: its CTAs take every SM
+  if (rc) return rc;
+  rc = launch_gemm_tc<256>(a, pt, f->side);
+  if (rc) return rc;
+  LP_CUDA_TRY(cudaEventRecord(f->join, f->side));
+  LP_CUDA_TRY(cudaStreamWaitEvent(st, f->join, 0));
+  return LP_OK;
+}
 
 int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
   LP_CHECK_ARG(num_sms() > 0, "lp_init() must be called before the tcgen05 GEMM");
@@ -529,6 +597,8 @@ int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
   if (a->m == 0) return LP_OK;
   GemmParams p;
   p.m = a->m;
+  p.m_begin = 0;
+  p.m_end = a->m;
   p.n = a->n;
   p.k = a->k;
   p.epilogue = a->epilogue;
@@ -556,8 +626,12 @@ int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
       const long sms = std::max(1, num_sms()), pairs = std::max(1L, sms / 2);
       const long waves2 = (((a->m + 255) / 256) * (a->n / 256) + pairs - 1) / pairs;
       const long waves1 = (((a->m + GBM - 1) / GBM) * (a->n / 256) + sms - 1) / sms;
-      if (g_gemm2 && g_gemm2_qkv && a->m >= 256 && (g_gemm2_all || waves2 * 23 < waves1 * 25))
-        return launch_gemm_tc2<256>(a, p, st);
+      const bool pair = g_gemm2 && g_gemm2_qkv && a->m >= 256 && (g_gemm2_all || waves2 * 23 < waves1 * 25);
+      if (g_gemm2_qkv) {
+        const int rc = launch_pair_split(a, p, st, pair ? waves2 : waves1, pair);
+        if (rc != 1) return rc;
+      }
+      if (pair) return launch_gemm_tc2<256>(a, p, st);
       return launch_gemm_tc<256>(a, p, st);
     }
     LP_CHECK_ARG(128 % p.qkv.head_dim == 0, "gemm_tc: head_dim must divide the tile");
@@ -577,7 +651,10 @@ int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
     // per-wave gain (O-proj / FFN-down at 14B: 6 pair waves vs 5 single waves)
     const long pairs = std::max(1L, sms / 2), tiles2 = ((a->m + 255) / 256) * (a->n / 256);
     const long waves2 = (tiles2 + pairs - 1) / pairs, waves1 = (tiles_m * (a->n / 256) + sms - 1) / sms;
-    if (g_gemm2 && a->m >= 256 && (g_gemm2_all || waves2 * 23 < waves1 * 25)) return launch_gemm_tc2<256>(a, p, st);
+    const bool pair = g_gemm2 && a->m >= 256 && (g_gemm2_all || waves2 * 23 < waves1 * 25);
+    const int rc = launch_pair_split(a, p, st, pair ? waves2 : waves1, pair);
+    if (rc != 1) return rc;
+    if (pair) return launch_gemm_tc2<256>(a, p, st);
     return launch_gemm_tc<256>(a, p, st);
   }
   if (a->n % 128 == 0) return launch_gemm_tc<128>(a, p, st);

@@ -187,9 +187,20 @@ class Forward:
             self.attn_ws_bytes = int(nb.value)
             if self.attn_ws_bytes:
                 self.attn_ws = torch.empty(self.attn_ws_bytes, dtype=torch.uint8, device=dev)
+        # side stream + events: bf16 GEMMs with a ragged last 256-row block run
+        # the pair tiles and the single-CTA tail concurrently (lp_gemm_args.fork)
+        self.fork = None if self.fp32 else L.fork_create()
         self.graph = None
         self.lock = threading.Lock()
         self.probe = None  # optional callable(tag, 'begin'|'end', stream) for per-kernel timing
+
+    def __del__(self):
+        fork, self.fork = getattr(self, "fork", None), None
+        if fork:
+            try:
+                L.load().lp_fork_destroy(fork)
+            except Exception:  # noqa: BLE001 - interpreter shutdown
+                pass
 
     # ------------------------------------------------------------ inputs ----
     def write_inputs(self, block_index: int, t_index: int, steps: int, segments, cur_row: int,
@@ -250,6 +261,7 @@ class Forward:
         args.a, args.w, args.c = a, w, c
         args.bias, args.gate = bias, gate
         args.qkv = C.pointer(qkv) if qkv is not None else None
+        args.fork = self.fork
         L.call("lp_gemm", C.byref(args), st)
 
     def _proj(self, st, a, m, k, w_t, n, c, ldc, epi, out_dtype=None, bias=0, gate=0, w_col0=0, qkv=None):

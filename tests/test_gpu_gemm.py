@@ -23,8 +23,18 @@ def _init():
     L.init_device(0)
 
 
-def _gemm(a, w_t, c, epi, out_dtype, bias=None, gate=None, qkv=None, in_dtype=L.LP_BF16):
+_FORK = []
+
+
+def _fork():
+    if not _FORK:
+        _FORK.append(L.fork_create())
+    return _FORK[0]
+
+
+def _gemm(a, w_t, c, epi, out_dtype, bias=None, gate=None, qkv=None, in_dtype=L.LP_BF16, fork=False):
     args = L.GemmArgs()
+    args.fork = _fork() if fork else None
     args.in_dtype, args.out_dtype, args.epilogue = in_dtype, out_dtype, epi
     args.m, args.k = a.shape
     args.n = w_t.shape[0] if in_dtype == L.LP_BF16 else w_t.shape[1]
@@ -71,6 +81,49 @@ def test_activation_epilogues(epi):
     assert rel_l2(c.float().cpu(), ref.cpu()) < 5e-3
 
 
+@pytest.mark.parametrize("m,k,n", [(600, 256, 512), (4680, 512, 1024), (300, 128, 15360 // 4)])
+def test_pair_split_with_side_stream_tail(monkeypatch, m, k, n):
+    # pair tiles on rows [0, 256 * floor(m / 256)), single-CTA tail rows on the
+    # fork's side stream: same results as one launch, for STORE and RESID
+    monkeypatch.setenv("LP_PAIR_SPLIT_ALL", "1")
+    a, w = _ab(m, k, n, 5)
+    ref = a.float() @ w.float().T
+    c32 = torch.full((m, n), float("nan"), device=DEV)
+    _gemm(a, w, c32, L.EPI_STORE, L.LP_F32, fork=True)
+    assert rel_l2(c32.cpu(), ref.cpu()) < 1e-5
+    h = torch.randn((m, n), device=DEV)
+    gate = torch.randn(n, device=DEV)
+    want = h + gate * ref
+    _gemm(a, w, h, L.EPI_RESID, L.LP_F32, gate=gate, fork=True)
+    assert rel_l2(h.cpu(), want.cpu()) < 1e-5
+    # and bitwise the same as the unsplit launch (same per-tile k order)
+    c_one = torch.zeros((m, n), device=DEV)
+    monkeypatch.delenv("LP_PAIR_SPLIT_ALL")
+    _gemm(a, w, c_one, L.EPI_STORE, L.LP_F32, fork=False)
+    assert torch.equal(c_one, c32)
+
+
+def test_pair_split_inside_graph_capture(monkeypatch):
+    monkeypatch.setenv("LP_PAIR_SPLIT_ALL", "1")
+    m, k, n = 1000, 256, 1024
+    a, w = _ab(m, k, n, 6)
+    c = torch.zeros((m, n), device=DEV)
+    args = L.GemmArgs()
+    args.in_dtype, args.out_dtype, args.epilogue = L.LP_BF16, L.LP_F32, L.EPI_STORE
+    args.m, args.n, args.k = m, n, k
+    args.lda, args.ldw, args.ldc = k, k, n
+    args.a, args.w, args.c = a.data_ptr(), w.data_ptr(), c.data_ptr()
+    args.fork = _fork()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+        L.call("lp_gemm", C.byref(args), s.cuda_stream)
+    c.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert rel_l2(c.cpu(), (a.float() @ w.float().T).cpu()) < 1e-5
+
+
 def test_gated_residual_epilogue():
     m, k, n = 250, 448, 256
     a, w = _ab(m, k, n, 2)
@@ -81,9 +134,11 @@ def test_gated_residual_epilogue():
     assert rel_l2(h.cpu(), ref.cpu()) < 1e-5
 
 
-@pytest.mark.parametrize("qk_norm,spatial,n_heads,frames", [(False, False, 4, 0), (True, True, 4, 3),
-                                                             (True, True, 8, 5)])
-def test_qkv_epilogue(qk_norm, spatial, n_heads, frames):
+@pytest.mark.parametrize("qk_norm,spatial,n_heads,frames,split", [(False, False, 4, 0, False),
+                                                                   (True, True, 4, 3, False),
+                                                                   (True, True, 8, 5, False),
+                                                                   (True, True, 8, 5, True)])
+def test_qkv_epilogue(monkeypatch, qk_norm, spatial, n_heads, frames, split):
     # m >= 256 takes the cluster-pair kernel (390 / 650 tokens: ragged last pair tile)
     hd = 128
     d = n_heads * hd
@@ -111,7 +166,9 @@ def test_qkv_epilogue(qk_norm, spatial, n_heads, frames):
     epi = L.QkvEpi(d, n_heads, hd, int(qk_norm), 1e-6, g_q.data_ptr() if qk_norm else 0,
                    g_k.data_ptr() if qk_norm else 0, q.data_ptr(), karena.data_ptr(), varena.data_ptr(),
                    ddev.data_ptr(), geom)
-    _gemm(a, w, None, L.EPI_QKV, L.LP_BF16, qkv=epi)
+    if split:
+        monkeypatch.setenv("LP_PAIR_SPLIT_ALL", "1")
+    _gemm(a, w, None, L.EPI_QKV, L.LP_BF16, qkv=epi, fork=split)
     y = a.float() @ w.float().T
     qr, kr, vr = y[:, :d], y[:, d:2 * d], y[:, 2 * d:]
 
