@@ -86,23 +86,31 @@ def test_flash_attention_matches_reference(case):
     assert torch.equal(tc, tc2)
 
 
-def test_segment_order_matters_only_through_content():
-    # permuting which physical rows hold the history changes nothing if the
-    # descriptor lists them in the same logical order
+def test_segments_are_visited_in_arena_order():
+    # softmax(QK^T)V does not depend on key order; the tcgen05 kernel walks
+    # the segments in arena-row order and merges adjacent ones, so the
+    # descriptor's logical order changes nothing (bitwise), and moving the
+    # same keys to other rows changes only the rounding
     heads, n_q, d = 2, 256, 256
     g = torch.Generator(device=DEV).manual_seed(9)
     ka = torch.randn((1500, d), generator=g, device=DEV).to(torch.bfloat16)
     va = torch.randn((1500, d), generator=g, device=DEV).to(torch.bfloat16)
     q = torch.randn((n_q, d), generator=g, device=DEV).to(torch.bfloat16)
+    scale = 0.0883883461356163
+    sa = [(0, 64), (300, 256), (556, 144), (700, 256), (1200, n_q)]
+    sb = [(0, 64), (700, 256), (556, 144), (300, 256), (1200, n_q)]
+    a = _run("lp_attention", q, ka, va, make_desc(3, sa, 1200, n_q, 128), heads, scale, 976)
+    b = _run("lp_attention", q, ka, va, make_desc(3, sb, 1200, n_q, 128), heads, scale, 976)
+    assert torch.equal(a, b)
+    # one merged range [300, 956) == the three adjacent segments
+    sc = [(0, 64), (300, 656), (1200, n_q)]
+    c = _run("lp_attention", q, ka, va, make_desc(3, sc, 1200, n_q, 128), heads, scale, 976)
+    assert torch.equal(a, c)
     kb, vb = ka.clone(), va.clone()
     kb[300:556], kb[700:956] = ka[700:956], ka[300:556]
     vb[300:556], vb[700:956] = va[700:956], va[300:556]
-    sa = [(0, 64), (300, 256), (700, 256), (1200, n_q)]
-    sb = [(0, 64), (700, 256), (300, 256), (1200, n_q)]
-    scale = 0.0883883461356163
-    a = _run("lp_attention", q, ka, va, make_desc(3, sa, 1200, n_q, 128), heads, scale, 832)
-    b = _run("lp_attention", q, kb, vb, make_desc(3, sb, 1200, n_q, 128), heads, scale, 832)
-    assert torch.equal(a, b)
+    e = _run("lp_attention", q, kb, vb, make_desc(3, sa, 1200, n_q, 128), heads, scale, 976)
+    assert rel_l2(e.float().cpu(), a.float().cpu()) < 1e-2
 
 
 @pytest.mark.parametrize("heads", [40, 12])
