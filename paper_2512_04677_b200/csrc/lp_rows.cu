@@ -386,6 +386,58 @@ __global__ void history_noise_kernel(T* __restrict__ arena, int d, const float* 
   }
 }
 
+// Perf-run variant (device RNG, bf16 arena): 8 elements per thread from one
+// Philox4x32-7 call -- each 32-bit word drives one Box-Muller pair (20-bit
+// radius uniform: tail cut at 5.4 sigma, P = 7e-8; 12-bit angle) -- with one
+// 16-byte load and store and 32-bit index math.  Half the RNG and index work
+// per element of history_noise_kernel; the parity path (host draws) is above.
+__device__ __forceinline__ void normal8_fast(uint64_t seed, uint64_t stream, uint32_t ctr, float* z) {
+  const uint4 c = make_uint4(ctr, 0x9E3779B9u, (uint32_t)stream, (uint32_t)(stream >> 32));
+  const uint2 k = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  const uint4 r = Philox::gen<7>(c, k);
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float u = ((float)(w[j] >> 12) + 0.5f) * 9.5367431640625e-07f;  // 2^-20
+    const float a = ((float)(w[j] & 0xFFFu) + 0.5f) * 1.5339807878856412e-03f;  // 2 pi / 4096
+    const float rad = sqrtf(-2.0f * __logf(u));
+    float sn, cs;
+    __sincosf(a, &sn, &cs);
+    z[2 * j] = rad * cs;
+    z[2 * j + 1] = rad * sn;
+  }
+}
+
+__global__ void history_noise_bf16x8_kernel(__nv_bfloat16* __restrict__ arena, int d, int layer, int kv,
+                                            const lp_block_desc* __restrict__ desc) {
+  const float sigma = desc->sigma;
+  const int n_hist = desc->n_seg - 2;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  int base = 0;
+  for (int e = 0; e < n_hist; ++e) {
+    const int s = e + 1;
+    const int len = desc->seg_len[s] * d;
+    if (i < base + len) {
+      const int off = i - base;  // multiple of 8; len is a multiple of d (of 8)
+      __nv_bfloat16* dst = arena + (int64_t)desc->seg_row[s] * d + off;
+      const __nv_bfloat16* src = arena + (int64_t)desc->src_row[s] * d + off;
+      float z[8];
+      normal8_fast(desc->noise_key, ((uint64_t)(layer * 2 + kv) << 8) | (uint64_t)e, (uint32_t)(off >> 3), z);
+      uint4 raw = *reinterpret_cast<const uint4*>(src);
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 x = __bfloat1622float2(h[j]);
+        h[j] = __floats2bfloat162_rn(__fadd_rn(x.x, __fmul_rn(z[2 * j], sigma)),
+                                     __fadd_rn(x.y, __fmul_rn(z[2 * j + 1], sigma)));
+      }
+      *reinterpret_cast<uint4*>(dst) = raw;
+      return;
+    }
+    base += len;
+  }
+}
+
 // ---------------------------------------------------------------- launch ---
 static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
@@ -406,6 +458,7 @@ int preload_rows() {
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, unpatchify_euler_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_kernel<float>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_kernel<__nv_bfloat16>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_bf16x8_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, randn_kernel<float>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, randn_kernel<__nv_bfloat16>));
   return LP_OK;
@@ -519,6 +572,10 @@ int history_noise(void* arena, int dtype, int d, const float* noise, int n_layer
   LP_CHECK_ARG(d % 4 == 0, "history_noise: d must be a multiple of 4");
   int64_t n = (int64_t)max_rows * d;
   if (n == 0) return LP_OK;
+  if (!noise && dtype == LP_BF16 && d % 8 == 0 && n < (1ll << 31)) {
+    history_noise_bf16x8_kernel<<<nblk(n / 8, 256), 256, 0, st>>>((__nv_bfloat16*)arena, d, layer, kv, desc);
+    return launch_status("history_noise");
+  }
   int blocks = nblk((n + 3) / 4, 256);
   if (dtype == LP_BF16)
     history_noise_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((__nv_bfloat16*)arena, d, noise, n_layers, layer,

@@ -16,5 +16,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s 2000 -c 4 -o $OUT/gemm $B > $OUT/ncu_gemm.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:norm_mod_kernel -s 1000 -c 1 -o $OUT/norm $B > $OUT/ncu_norm.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:sink_refresh_t_kernel -s 2 -c 1 -o $OUT/sink $B > $OUT/ncu_sink.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:history_noise_kernel -s 700 -c 1 -o $OUT/hist $B --history-sigma 0.1 > $OUT/ncu_hist.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:history_noise -s 700 -c 1 -o $OUT/hist $B --history-sigma 0.1 > $OUT/ncu_hist.log 2>&1
 ls -la $OUT

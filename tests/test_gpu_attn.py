@@ -164,4 +164,7 @@ def test_device_history_noise_moments(dtype):
     z = (arena[1200:1200 + n_tok].float() - 1.0) / sigma
     assert abs(float(z.mean())) < 0.02
     assert abs(float(z.std()) - 1.0) < 0.05
+    kurt = float(((z - z.mean()) ** 4).mean() / z.var() ** 2)
+    assert abs(kurt - 3.0) < 0.1, kurt
+    assert abs(float((z.abs() > 2.0).float().mean()) - 0.0455) < 0.003  # two-sided 2-sigma tail
     assert torch.all(arena[0:n_tok] == 1.0)  # stored ring untouched
