@@ -449,6 +449,8 @@ int preload_rows() {
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<float, 128, 4>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<__nv_bfloat16, 128, 4>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<__nv_bfloat16, 256>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<__nv_bfloat16, 128, 10>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<float, 128, 10>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, sink_refresh_kernel<float>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, sink_refresh_kernel<__nv_bfloat16>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, sink_refresh_t_kernel<float>));
@@ -488,6 +490,12 @@ int norm_mod(const float* h, int rows, int d, int mode, float eps, const float* 
                                                                    (__nv_bfloat16*)out);
     else
       norm_mod_kernel<float, 128, 4><<<rows, 128, 0, st>>>(h, d, mode, eps, shift, scale, (float*)out);
+  } else if (d <= 128 * 4 * 10) {  // 14B (d = 5120): 128 threads, 10 float4 per thread (6-8 % over 256 x 5)
+    if (out_dtype == LP_BF16)
+      norm_mod_kernel<__nv_bfloat16, 128, 10><<<rows, 128, 0, st>>>(h, d, mode, eps, shift, scale,
+                                                                     (__nv_bfloat16*)out);
+    else
+      norm_mod_kernel<float, 128, 10><<<rows, 128, 0, st>>>(h, d, mode, eps, shift, scale, (float*)out);
   } else if (out_dtype == LP_BF16) {
     norm_mod_kernel<__nv_bfloat16, 256><<<rows, 256, 0, st>>>(h, d, mode, eps, shift, scale,
                                                                (__nv_bfloat16*)out);

@@ -236,3 +236,27 @@ def test_euler_epilogue(patched):
     torch.cuda.synchronize()
     ref = x_in + vu * dt
     assert rel_l2(x_out.cpu(), ref.cpu()) < 1e-5
+
+
+@pytest.mark.parametrize("d", [256, 1536, 5120, 6144])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_norm_mod_rows(d, mode):
+    # pre-LN + AdaLN row kernel at the 1.3B / 14B widths and a wider
+    # re-read one: out = LN(h) * (1 + scale) + shift (mode 2), LN(h) (1), copy (0)
+    rows = 37
+    g = torch.Generator(device=DEV).manual_seed(d + mode)
+    h = torch.randn((rows, d), generator=g, device=DEV) * 3 + 0.5
+    sh, sc = torch.randn(d, generator=g, device=DEV), torch.randn(d, generator=g, device=DEV)
+    if mode == 0:
+        ref = h
+    else:
+        ref = torch.nn.functional.layer_norm(h.double(), (d,), eps=1e-6).float()
+        if mode == 2:
+            ref = ref * (1 + sc) + sh
+    st = torch.cuda.current_stream().cuda_stream
+    for dt, tol in ((torch.float32, 1e-5), (torch.bfloat16, 5e-3)):
+        out = torch.empty((rows, d), device=DEV, dtype=dt)
+        L.call("lp_norm_mod", h.data_ptr(), rows, d, mode, 1e-6, sh.data_ptr(), sc.data_ptr(), out.data_ptr(),
+               L.LP_F32 if dt == torch.float32 else L.LP_BF16, st)
+        torch.cuda.synchronize()
+        assert rel_l2(out.float().cpu(), ref.cpu()) < tol, (d, mode, dt)
