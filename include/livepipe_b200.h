@@ -165,6 +165,9 @@ LP_API int lp_gemm(const lp_gemm_args* args, void* stream);
    stream capture, one per concurrently used stream.                        */
 LP_API int lp_fork_create(void** out);
 LP_API int lp_fork_destroy(void* fork);
+/* Kernel nodes of a captured CUDA graph (cudaGraph_t as void*): the exact
+   number of kernels one replay launches (bench.py's gpu_launches claim).  */
+LP_API int lp_graph_kernel_count(void* graph, int64_t* count);
 
 /* ---------------------------------------------------------------- attention
  * replaces the per-head loop of denoise_block (denoiser.py:246-264) and

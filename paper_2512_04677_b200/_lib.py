@@ -92,6 +92,7 @@ _SIGS = {
                             C.c_int),
     "lp_fork_create": ([C.POINTER(vp)], C.c_int),
     "lp_fork_destroy": ([vp], C.c_int),
+    "lp_graph_kernel_count": ([vp, C.POINTER(C.c_int64)], C.c_int),
     "lp_codec_patch_decode": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, vp],
                               C.c_int),
     "lp_codec_patch_encode": ([vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp], C.c_int),
@@ -160,6 +161,13 @@ def fork_create() -> int:
     h = C.c_void_p()
     call("lp_fork_create", C.byref(h))
     return h.value
+
+
+def graph_kernel_count(graph) -> int:
+    """Kernel nodes of a captured torch.cuda.CUDAGraph (exact launches per replay)."""
+    n = C.c_int64(0)
+    call("lp_graph_kernel_count", C.c_void_p(int(graph.raw_cuda_graph())), C.byref(n))
+    return int(n.value)
 
 
 def init_device(device: int) -> None:

@@ -1,6 +1,7 @@
 // extern "C" surface of liblivepipe_b200.so (declared in include/livepipe_b200.h).
 #include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "lp_common.cuh"
 #include "lp_tma.cuh"
@@ -212,6 +213,23 @@ int lp_link_recv(const void* src_slot, void* dst, int64_t bytes, volatile const 
 int lp_fork_create(void** out) { return fork_create(out); }
 
 int lp_fork_destroy(void* fork) { return fork_destroy(fork); }
+
+int lp_graph_kernel_count(void* graph, int64_t* count) {
+  LP_CHECK_ARG(graph && count, "lp_graph_kernel_count: null argument");
+  cudaGraph_t g = static_cast<cudaGraph_t>(graph);
+  size_t n = 0;
+  LP_CUDA_TRY(cudaGraphGetNodes(g, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (n) LP_CUDA_TRY(cudaGraphGetNodes(g, nodes.data(), &n));
+  int64_t k = 0;
+  for (size_t i = 0; i < n; ++i) {
+    cudaGraphNodeType t;
+    LP_CUDA_TRY(cudaGraphNodeGetType(nodes[i], &t));
+    if (t == cudaGraphNodeTypeKernel) ++k;
+  }
+  *count = k;
+  return LP_OK;
+}
 
 int lp_codec_patch_decode(const float* x, int frames, int C, int H, int W, const float* maps, int r, int pc, int s,
                           float* out, void* stream) {

@@ -281,9 +281,11 @@ class Stage:
         if not self.use_graph or self.graph is not None:
             return
         with torch.cuda.device(self.device):
-            g = torch.cuda.CUDAGraph()
+            g = torch.cuda.CUDAGraph(keep_graph=True)
             with torch.cuda.graph(g, stream=self.stream, capture_error_mode="thread_local"):
                 self.fw.launch(stream=self.stream)
+            self.fw.graph_kernels = L.graph_kernel_count(g)
+            g.instantiate()
             self.graph = g
 
     def ensure_out_graphs(self, out_ptrs) -> None:
@@ -295,9 +297,11 @@ class Stage:
             if ptr in self.out_graphs:
                 continue
             with torch.cuda.device(self.device):
-                g = torch.cuda.CUDAGraph()
+                g = torch.cuda.CUDAGraph(keep_graph=True)
                 with torch.cuda.graph(g, stream=self.stream, capture_error_mode="thread_local"):
                     self.fw.launch(stream=self.stream, x_out=int(ptr))
+                self.fw.graph_kernels = L.graph_kernel_count(g)
+                g.instantiate()
                 self.out_graphs[ptr] = g
 
     def forward(self, i: int, timed: bool = True, out_ptr: int | None = None) -> None:

@@ -476,8 +476,15 @@ class Forward:
         self._sigma_on = bool(on)
         self.noise = noise
 
+    graph_kernels = None  # kernel nodes of the captured forward graph (exact, set on capture)
+
     def kernels_per_forward(self) -> int:
-        """Number of kernel launches ``launch`` enqueues (gpu_launches claim)."""
+        """Number of kernel launches ``launch`` enqueues (gpu_launches claim):
+        the captured graph's kernel-node count when there is one (it includes
+        the side-stream tail GEMMs of lp_gemm's pair split), else the count
+        of launch() call sites."""
+        if self.graph_kernels is not None:
+            return self.graph_kernels
         prof = self.prof
         n = 1 + 1 + 1  # cond_row, embed add (toy) or 3 (patched), sink refresh
         if prof.patched:

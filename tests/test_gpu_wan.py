@@ -126,3 +126,19 @@ def test_long_horizon_stream_device_noise():
             v = x.float()
             assert torch.isfinite(v).all() and float(v.abs().max()) < 1e3
     assert all(st.nfe == n_blocks for st in pipe.stages.values())
+
+
+def test_graph_kernel_count_matches_launch_sites():
+    # gpu_launches claim: kernel nodes of the captured forward graph; without
+    # a pair split (small M) they equal the launch() call-site count
+    _, pp = _profiles()
+    cfg = lp.EngineConfig(mode="sequential", profile=pp, precision="bf16", steps=2, blocks=2, cache_capacity=2)
+    pipe = lp.StreamingPipeline(cfg)
+    noise = torch.from_numpy(lp.noise_block(cfg, 0).values).cuda()
+    pipe.submit(0, noise)
+    pipe.capture()
+    torch.cuda.synchronize()
+    for st in pipe.stages.values():
+        n_graph = st.fw.kernels_per_forward()
+        st.fw.graph_kernels = None
+        assert n_graph == st.fw.kernels_per_forward()
