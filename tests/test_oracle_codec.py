@@ -56,3 +56,13 @@ def test_patch_codec_geometry_errors():
         PatchVideoCodec(7, 16, 4, 4, upsample=0)
     with pytest.raises(ValueError):
         ToyVideoCodec(7, 16, 8, 4)
+
+
+def test_engine_config_codec_fields():
+    import paper_2512_04677_b200 as lp
+
+    for bad in (dict(pixel_scale=0), dict(pixel_channels=0), dict(upsample=0)):
+        with pytest.raises(lp.EngineConfigError):
+            lp.EngineConfig(**bad)
+    cfg = lp.EngineConfig(patch_codec=True, pixel_channels=3, pixel_scale=8)
+    assert cfg.patch_codec and cfg.pixel_scale == 8
