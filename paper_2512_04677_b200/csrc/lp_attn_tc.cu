@@ -46,6 +46,10 @@ namespace lp {
 
 using namespace sm100;
 
+#ifndef LP_ATTN_POLY
+#define LP_ATTN_POLY 3  // pairs of every 8 whose exp2 runs as the FMA-pipe polynomial (sweep: r1c, r1j)
+#endif
+
 constexpr int AT_M = 128;      // query rows per softmax warpgroup
 constexpr int AT_N = 128;      // keys per tile
 constexpr int AT_D = 128;      // head dim
@@ -479,7 +483,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       auto exp_pairs = [&](int i0) {
 #pragma unroll
         for (int i = i0; i < i0 + 64; i += 2) {
-          const bool poly = ((i >> 1) & 7) >= 5;
+          const bool poly = ((i >> 1) & 7) >= 8 - LP_ATTN_POLY;
           const uint64_t a = ffma2(f32x2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sc2, nm2);
           uint64_t e;
           if (poly) {
