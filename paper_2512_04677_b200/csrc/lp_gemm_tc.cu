@@ -44,6 +44,20 @@ struct ForkCtx {
   cudaEvent_t fork, join;
 };
 
+// Tile raster: groups of LP_GEMM_GROUP row blocks, column-major inside a
+// group, so a wave of ~148 (74 pair) tiles covers a compact block of rows x
+// columns and both operands are re-read from L2 rather than DRAM.
+#ifndef LP_GEMM_GROUP
+#define LP_GEMM_GROUP 16
+#endif
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& mb, int& nb) {
+  const int per = LP_GEMM_GROUP * tiles_n;
+  const int g = tile / per, r = tile - g * per;
+  const int gm = min(LP_GEMM_GROUP, tiles_m - g * LP_GEMM_GROUP);
+  mb = g * LP_GEMM_GROUP + r % gm;
+  nb = r / gm;
+}
+
 template <int BN>
 struct GemmSmem {
   static constexpr int A_BYTES = GBM * GBK * 2;
@@ -261,7 +275,9 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       uint32_t phase = 0;
       const uint64_t pol_a = l2_policy_evict_last();
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = p.m_begin + (tile % tiles_m) * GBM, n0 = (tile / tiles_m) * BN;
+        int mb, nb;
+        tile_coords(tile, tiles_m, tiles_n, mb, nb);
+        const int m0 = p.m_begin + mb * GBM, n0 = nb * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * SM::STAGE_BYTES;
@@ -316,7 +332,9 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int acc = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
-      const int m0 = p.m_begin + (tile % tiles_m) * GBM, n0 = (tile / tiles_m) * BN;
+      int mb, nb;
+      tile_coords(tile, tiles_m, tiles_n, mb, nb);
+      const int m0 = p.m_begin + mb * GBM, n0 = nb * BN;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int row = m0 + quarter * 32 + lane;
@@ -402,9 +420,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
       uint32_t phase = 0;
       const uint64_t pol = l2_policy_evict_last();
       for (int tile = cid; tile < num_tiles; tile += nclu) {
-        int m0 = p.m_begin + (tile % tiles_m) * 2 * GBM + rank * GBM;
+        int mb, nb;
+        tile_coords(tile, tiles_m, tiles_n, mb, nb);
+        int m0 = p.m_begin + mb * 2 * GBM + rank * GBM;
         if (m0 >= p.m) m0 = p.m > GBM ? p.m - GBM : 0;  // wholly past M: load valid rows, results discarded
-        const int n0 = (tile / tiles_m) * BN + rank * (BN / 2);
+        const int n0 = nb * BN + rank * (BN / 2);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * SM::STAGE_BYTES;
@@ -461,7 +481,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
     for (int tile = cid; tile < num_tiles; tile += nclu, ++local) {
       const int acc = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
-      const int m0 = p.m_begin + (tile % tiles_m) * 2 * GBM + rank * GBM, n0 = (tile / tiles_m) * BN;
+      int mb, nb;
+      tile_coords(tile, tiles_m, tiles_n, mb, nb);
+      const int m0 = p.m_begin + mb * 2 * GBM + rank * GBM, n0 = nb * BN;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int row = m0 + quarter * 32 + lane;
