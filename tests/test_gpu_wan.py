@@ -142,3 +142,18 @@ def test_graph_kernel_count_matches_launch_sites():
         n_graph = st.fw.kernels_per_forward()
         st.fw.graph_kernels = None
         assert n_graph == st.fw.kernels_per_forward()
+
+
+def test_tpp_with_pair_split_bitwise_equals_sequential(monkeypatch):
+    # 288 tokens per block: the GEMMs run pair tiles on rows [0, 256) and the
+    # ragged 32 rows on each stage's fork side stream (forced here), inside
+    # the captured graphs of 4 concurrently running stage threads
+    monkeypatch.setenv("LP_PAIR_SPLIT_ALL", "1")
+    _, pp = _profiles(layers=2, heads=2, ffn=512, h=16, w=24)
+    kw = dict(steps=4, blocks=4, cache_capacity=2)
+    seq = _engine(pp, "bf16", **kw)
+    tpp = _engine(pp, "bf16", mode="tpp", **kw)
+    assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(seq.blocks, tpp.blocks))
+    monkeypatch.delenv("LP_PAIR_SPLIT_ALL")
+    plain = _engine(pp, "bf16", **kw)  # the split changes no bits either
+    assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(seq.blocks, plain.blocks))
