@@ -260,3 +260,20 @@ def test_norm_mod_rows(d, mode):
                L.LP_F32 if dt == torch.float32 else L.LP_BF16, st)
         torch.cuda.synchronize()
         assert rel_l2(out.float().cpu(), ref.cpu()) < tol, (d, mode, dt)
+
+
+def test_argument_errors_are_reported_not_launched():
+    # the C ABI validates before launching and returns LP_EINVAL with a message
+    a, w = _ab(128, 100, 256)  # k not a multiple of 64 (bf16 tcgen05 path)
+    c = torch.zeros((128, 256), device=DEV)
+    with pytest.raises(L.LivepipeError, match="multiple of 64"):
+        _gemm(a, w, c, L.EPI_STORE, L.LP_F32)
+    a, w = _ab(128, 128, 100)  # n not a multiple of 64
+    c = torch.zeros((128, 100), device=DEV)
+    with pytest.raises(L.LivepipeError, match="multiple of 64"):
+        _gemm(a, w, c, L.EPI_STORE, L.LP_F32)
+    with pytest.raises(L.LivepipeError, match="null"):
+        L.call("lp_codec_patch_decode", None, 1, 16, 2, 2, None, 1, 3, 8, None, None)
+    with pytest.raises(L.LivepipeError, match="channels"):
+        x = torch.zeros(64, device=DEV)
+        L.call("lp_codec_patch_decode", x.data_ptr(), 1, 64, 1, 1, x.data_ptr(), 1, 3, 8, x.data_ptr(), None)
