@@ -158,26 +158,39 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(q) + (__float_as_int(t) << 23));
 }
 
-// Walks the KV tiles of the descriptor's segments in order.
+// Walks the KV tiles of the (merged, arena-ordered) segments.  The segment
+// table lives in shared memory and is read through 32-bit shared addresses
+// (ld.shared): a generic int* here compiled to LD.E through a 64-bit pointer
+// that the softmax warpgroups spilled and reloaded every tile.
+__device__ __forceinline__ int lds_s32(uint32_t addr) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
 struct TileCursor {
-  const int* row;
-  const int* len;
-  int n_seg, seg, off;
+  uint32_t row_s, len_s;  // shared addresses of seg_row[0], seg_len[0]
+  int n_seg, seg, off, len, row;
+  __device__ void load() {
+    row = lds_s32(row_s + 4u * seg);
+    len = lds_s32(len_s + 4u * seg);
+  }
   __device__ void init(const int* r, const int* l, int n) {
-    row = r; len = l; n_seg = n; seg = 0; off = 0;
-    while (seg < n_seg && len[seg] == 0) ++seg;
+    row_s = (uint32_t)__cvta_generic_to_shared(r);
+    len_s = (uint32_t)__cvta_generic_to_shared(l);
+    n_seg = n; seg = 0; off = 0; len = 0; row = 0;
+    if (n_seg > 0) load();
   }
   __device__ void skip(int tiles) {
     for (int i = 0; i < tiles; ++i) next();
   }
-  __device__ int cur_row() const { return row[seg] + off; }
-  __device__ int cur_valid() const { return min(AT_N, len[seg] - off); }
+  __device__ int cur_row() const { return row + off; }
+  __device__ int cur_valid() const { return min(AT_N, len - off); }
   __device__ void next() {
     off += AT_N;
-    if (off >= len[seg]) {
+    if (off >= len) {
       off = 0;
-      ++seg;
-      while (seg < n_seg && len[seg] == 0) ++seg;
+      if (++seg < n_seg) load();
     }
   }
 };
