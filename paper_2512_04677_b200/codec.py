@@ -38,8 +38,8 @@ class DeviceCodec:
         if isinstance(codec, ToyVideoCodec):
             self.kind = "dense"
             # fp32 lp_gemm takes W as (k, n) row-major: the transposed maps
-            self.maps_t = [torch.from_numpy(np.ascontiguousarray(m.T)).to(dev) for m in codec._decode_maps]
-            self.enc_t = torch.from_numpy(np.ascontiguousarray(codec._encode_map.T)).to(dev)
+            self.maps_t = [torch.from_numpy(np.ascontiguousarray(m.T)).to(dev) for m in codec.decode_maps]
+            self.enc_t = torch.from_numpy(np.ascontiguousarray(codec.encode_map.T)).to(dev)
         elif isinstance(codec, PatchVideoCodec):
             self.kind = "patch"
             self.maps = torch.from_numpy(np.ascontiguousarray(codec.maps)).to(dev)
