@@ -368,6 +368,10 @@ def run_ours(args):
                    "frac_of_burst_peak": ach / burst_tf,
                    "roofline_fps_sustained": FRAMES_PER_BLOCK_VIDEO / (flops_block / (peak_tf * 1e12)),
                    "roofline_fps_burst": FRAMES_PER_BLOCK_VIDEO / (flops_block / (burst_tf * 1e12)),
+                   "frac_of_roofline_fps_sustained": fps / (FRAMES_PER_BLOCK_VIDEO / (flops_block / (peak_tf * 1e12))),
+                   "ttff_ms_estimate": ms_step + decode_stage["ms_per_block"],
+                   "ttff_note": "N=1, graphs captured: block 0 passes all T steps (one block latency) then the "
+                                "decode stage; arrival offset 0",
                    "probe_block_ms": probe_ms},
         "e2e": {"value": e2e_fps, "unit": "FPS", "h2d_bytes_per_step": 3 * lat * 4,
                 "d2h_bytes_per_step": 3 * lat * 4, "wall_s": wall_e2e},
