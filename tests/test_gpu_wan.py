@@ -157,3 +157,16 @@ def test_tpp_with_pair_split_bitwise_equals_sequential(monkeypatch):
     monkeypatch.delenv("LP_PAIR_SPLIT_ALL")
     plain = _engine(pp, "bf16", **kw)  # the split changes no bits either
     assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(seq.blocks, plain.blocks))
+
+
+@pytest.mark.parametrize("precision,tol", [("bf16", TOL_BF16), ("fp32", TOL_FP32)])
+def test_wan_clean_kv_matches_oracle(precision, tol):
+    # the clean-cache baseline (engine.py:292-331) on the Wan profile through
+    # the drop-in denoiser: T noisy steps + one level-0 cache pass per block
+    po, pp = _profiles()
+    kw = dict(steps=3, blocks=4, cache_capacity=2)
+    ref, _, nfe = O.run_clean_kv(O.RolloutCfg(profile=po, **kw), mm=O.mm_f64, codec=False)
+    res = lp.run(lp.EngineConfig(mode="clean_kv", profile=pp, precision=precision, **kw))
+    assert res.nfe == nfe == 4 * (3 + 1)
+    errs = [rel_l2(b.values, r) for b, r in zip(res.blocks, ref)]
+    assert max(errs) < tol, errs
