@@ -228,6 +228,15 @@ class Stage:
             self.fw = Forward(dw, cfg.frames_per_block, self.arena)
             self.fw.sink_v_static = True  # sink rows fixed at [0, S) (write_inputs sink_row=0)
         self.fw.set_history_noise(self.sigma_on, None)
+        self._noise_host = self._noise_dev = self._noise_ev = None
+        if self.sigma_on and not cfg.device_inputs:
+            # parity runs upload the reference's host draws every call: fixed
+            # pinned + device buffers, so no allocation (which may synchronise
+            # the device) happens while another stage's link kernel spins
+            shape = (self.L, 2, prof.n_layers, n_tok, prof.model_dim)
+            self._noise_host = torch.empty(shape, dtype=torch.float32).pin_memory()
+            with torch.cuda.device(device):
+                self._noise_dev = torch.empty(shape, dtype=torch.float32, device=f"cuda:{device}")
         self.ring = RingIndex(self.L)  # RollingKvCache replay on ring slots (kvcache.py:41-56)
         self.graph = None
         self.nfe = 0
@@ -254,9 +263,19 @@ class Stage:
             g = corruption_prng(cfg.noise_seed, i, self.j)
             prof = cfg.model_profile
             shape = (ar.n_tokens, prof.model_dim)
-            arr = np.stack([np.stack([np.stack([g.normal(shape) for _ in range(prof.n_layers)])
-                                      for _kv in range(2)]) for _ in self.ring.blocks])
-            noise = torch.from_numpy(arr).to(f"cuda:{self.device}")
+            n = len(self.ring)
+            if self._noise_ev is not None:
+                self._noise_ev.synchronize()  # the previous upload has left the pinned buffer
+            host = self._noise_host[:n].numpy()
+            for e in range(n):
+                for kv in range(2):
+                    for layer in range(prof.n_layers):
+                        host[e, kv, layer] = g.normal(shape)
+            with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+                self._noise_dev[:n].copy_(self._noise_host[:n], non_blocking=True)
+                self._noise_ev = torch.cuda.Event()
+                self._noise_ev.record(self.stream)
+            noise = self._noise_dev[:n]
         if self.sigma_on:
             self._noise_keep = noise
             fw.noise = noise

@@ -170,3 +170,17 @@ def test_wan_clean_kv_matches_oracle(precision, tol):
     assert res.nfe == nfe == 4 * (3 + 1)
     errs = [rel_l2(b.values, r) for b, r in zip(res.blocks, ref)]
     assert max(errs) < tol, errs
+
+
+@pytest.mark.parametrize("mode", ["fixed", "scaled"])
+def test_wan_history_noise_bf16_matches_oracle_and_tpp(mode):
+    # corrupted cache views (kvcache.py:121-137) with the reference's host
+    # draws: bf16 within the bar against the oracle, and TPP bitwise equal to
+    # sequential under corruption (reference tests/test_engine.py:185-194)
+    po, pp = _profiles(layers=1)
+    kw = dict(steps=3, blocks=4, cache_capacity=2, history_sigma=0.2, history_mode=mode)
+    ref = _oracle(po, **kw)
+    seq = _engine(pp, "bf16", **kw)
+    assert max(rel_l2(b.values, r) for b, r in zip(seq.blocks, ref)) < TOL_BF16
+    tpp = _engine(pp, "bf16", mode="tpp", **kw)
+    assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(seq.blocks, tpp.blocks))
