@@ -285,20 +285,29 @@ class Forward:
         prof, dw = self.prof, self.dw
         st = (stream if stream is not None else torch.cuda.current_stream(self.device)).cuda_stream
         d, S = prof.model_dim, prof.tokens_per_frame
-        sink = torch.empty((1, prof.latent_dim), dtype=torch.float32, device=self.device)
+        # scratch allocated on the first call (before any stream runs) and
+        # reused: the RSFM swap arrives mid-stream in TPP, when another
+        # stage's link kernel may be spinning, and must not allocate
+        if getattr(self, "_sink_scratch", None) is None:
+            dev = self.device
+            self._sink_scratch = (
+                torch.empty((1, prof.latent_dim), dtype=torch.float32, device=dev),
+                torch.empty((S, prof.patch_dim), dtype=dw.dtype, device=dev) if prof.patched else None,
+                torch.empty((S, d), dtype=torch.float32, device=dev) if prof.patched else None,
+                torch.empty((S, d), dtype=dw.dtype, device=dev))
+        sink, tok, sh, xs = self._sink_scratch
         s_obj = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if getattr(self, "_sink_ev", None) is not None:
+            self._sink_ev.synchronize()
         self._sink_ev = h2d(sink, sink_frame.reshape(1, prof.latent_dim).float(), s_obj)
         self._sink_frame = sink
         if prof.patched:
-            tok = torch.empty((S, prof.patch_dim), dtype=dw.dtype, device=self.device)
             L.call("lp_patchify", sink.data_ptr(), 1, prof.channels, prof.height, prof.width, prof.patch[0],
                    prof.patch[1], tok.data_ptr(), dw.ldt, st)
-            sh = torch.empty((S, d), dtype=torch.float32, device=self.device)
             self._proj(st, tok.data_ptr(), S, prof.patch_dim, dw.w_emb, d, sh.data_ptr(), d, L.EPI_STORE,
                        L.LP_F32, bias=_p(dw.b_emb))
         else:
             sh = sink
-        xs = torch.empty((S, d), dtype=dw.dtype, device=self.device)
         L.call("lp_norm_mod", sh.data_ptr(), S, d, 1 if prof.pre_ln else 0, prof.eps, None, None, xs.data_ptr(),
                dw.ldt, st)
         for l in range(prof.n_layers):
