@@ -49,3 +49,14 @@ def test_ipc_tpp_with_decode_rank(tmp_path):
     got = np.load(f"{out}.0.npy")
     seq = lp.run_sequential(lp.EngineConfig(mode="sequential", **kw))
     assert got.tobytes() == np.stack([b.values for b in seq.blocks]).tobytes()
+
+
+def test_ipc_tpp_bf16_wan_history_noise_equals_sequential(tmp_path):
+    # corrupted views with the reference's host draws across ranks (parity
+    # noise uploads into fixed buffers while peer link kernels spin)
+    kw = dict(steps=4, blocks=4, cache_capacity=2, history_sigma=0.2, history_mode="scaled")
+    out = tmp_path / "res"
+    launch(4, "gpu", out, dict(kw, precision="bf16", profile="wan_small", link_timeout_s=60.0), timeout=600)
+    got = np.load(f"{out}.0.npy")
+    seq = lp.run_sequential(lp.EngineConfig(mode="sequential", precision="bf16", profile=wan_small(), **kw))
+    assert got.tobytes() == np.stack([b.values for b in seq.blocks]).tobytes()
