@@ -184,3 +184,14 @@ def test_wan_history_noise_bf16_matches_oracle_and_tpp(mode):
     assert max(rel_l2(b.values, r) for b, r in zip(seq.blocks, ref)) < TOL_BF16
     tpp = _engine(pp, "bf16", mode="tpp", **kw)
     assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(seq.blocks, tpp.blocks))
+
+
+def test_wan_clean_kv_with_corruption_bf16_matches_oracle():
+    # the drop-in denoiser with corrupt_history views (device entries carry
+    # the reference's host draws; noise added into scratch rows on the GPU)
+    po, pp = _profiles(layers=1)
+    kw = dict(steps=3, blocks=4, cache_capacity=2, history_sigma=0.2)
+    ref, _, nfe = O.run_clean_kv(O.RolloutCfg(profile=po, **kw), mm=O.mm_f64, codec=False)
+    res = lp.run(lp.EngineConfig(mode="clean_kv", profile=pp, precision="bf16", **kw))
+    assert res.nfe == nfe
+    assert max(rel_l2(b.values, r) for b, r in zip(res.blocks, ref)) < TOL_BF16
