@@ -195,3 +195,14 @@ def test_wan_clean_kv_with_corruption_bf16_matches_oracle():
     res = lp.run(lp.EngineConfig(mode="clean_kv", profile=pp, precision="bf16", **kw))
     assert res.nfe == nfe
     assert max(rel_l2(b.values, r) for b, r in zip(res.blocks, ref)) < TOL_BF16
+
+
+def test_1p3b_shape_tpp_bitwise_equals_sequential():
+    # the named 1.3B/480p shape (30 layers, d 1536, 4680 tokens per block,
+    # device-RNG weights): the pair + side-stream tail GEMMs, the KV-split
+    # attention grid and the fused Euler epilogue under 4 concurrent stages
+    kw = dict(profile=lp.WAN_1_3B, precision="bf16", steps=4, cache_capacity=2, blocks=4, device_inputs=True)
+    seq = lp.run(lp.EngineConfig(mode="sequential", **kw))
+    tpp = lp.run(lp.EngineConfig(mode="tpp", **kw))
+    assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(seq.blocks, tpp.blocks))
+    assert all(np.isfinite(b.values).all() for b in seq.blocks)
