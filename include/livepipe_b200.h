@@ -83,6 +83,14 @@ typedef struct lp_block_desc {
   float rope_sin[LP_MAX_PAIRS];
   float sink_cos[LP_MAX_PAIRS];
   float sink_sin[LP_MAX_PAIRS];
+  /* 1: the tcgen05 attention may visit the segments in arena-row order with
+     adjacent ones merged (fewer ragged tiles; the rounding then depends on
+     where the rows sit -- used by the engines, whose ring slots are a
+     function of the block index).  0: logical order, segment by segment,
+     so the result does not depend on row placement (the drop-in denoiser,
+     whose per-call K/V pool slots vary).  The fp32 path is always logical. */
+  int32_t arena_order;
+  int32_t reserved_;
 } lp_block_desc;
 
 /* Static rotary geometry of one model (per-head pair layout). */

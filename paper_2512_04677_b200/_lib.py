@@ -37,6 +37,7 @@ class BlockDesc(C.Structure):
         ("dt", f32), ("sigma", f32), ("noise_key", u64),
         ("rope_cos", f32 * MAX_PAIRS), ("rope_sin", f32 * MAX_PAIRS),
         ("sink_cos", f32 * MAX_PAIRS), ("sink_sin", f32 * MAX_PAIRS),
+        ("arena_order", i32), ("reserved_", i32),
     ]
 
 

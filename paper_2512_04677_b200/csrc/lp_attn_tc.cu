@@ -246,18 +246,21 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   const bool two = q0 + AT_M < p.n_q;  // tile B holds valid rows
 
   if (threadIdx.x == 0) {
-    // Key order does not change softmax(QK^T)V, so the segments are visited
-    // in arena-row order with physically adjacent ones merged: in steady
-    // state [sink | L+1 ring slots] is one contiguous range and only its last
-    // tile is ragged (24,960 keys: 195 tiles instead of 198 segment-by-
-    // segment).  Deterministic, and the same for every stage (TPP == seq).
+    // Key order does not change softmax(QK^T)V, so with desc->arena_order
+    // the segments are visited in arena-row order with physically adjacent
+    // ones merged: in steady state [sink | L+1 ring slots] is one contiguous
+    // range and only its last tile is ragged (24,960 keys: 195 tiles instead
+    // of 198 segment-by-segment).  Deterministic for a given row placement
+    // (the engines' ring slots depend only on the block index: TPP == seq);
+    // without it, logical order, so the drop-in's pool placement is invisible.
     const int n_in = min(p.desc->n_seg, LP_MAX_SEG);
+    const bool by_row = p.desc->arena_order != 0;
     int nseg = 0;
     for (int s = 0; s < n_in; ++s) {
       const int r = p.desc->seg_row[s], l = p.desc->seg_len[s];
       if (l <= 0) continue;
       int i = nseg++;
-      while (i > 0 && seg_row[i - 1] > r) {
+      while (by_row && i > 0 && seg_row[i - 1] > r) {
         seg_row[i] = seg_row[i - 1];
         seg_len[i] = seg_len[i - 1];
         --i;
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     }
     int merged = 0;
     for (int s = 0; s < nseg; ++s) {
-      if (merged > 0 && seg_row[merged - 1] + seg_len[merged - 1] == seg_row[s]) {
+      if (by_row && merged > 0 && seg_row[merged - 1] + seg_len[merged - 1] == seg_row[s]) {
         seg_len[merged - 1] += seg_len[s];
       } else {
         seg_row[merged] = seg_row[s];

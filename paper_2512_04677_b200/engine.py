@@ -283,7 +283,7 @@ class Stage:
         fw.write_inputs(i, self.j, cfg.steps, segs, ar.slot_row(self.ring.write_slot(i)),
                         rolling_rope_index(i, cfg.sink_delta), self.rt.schedule.dt,
                         self.rt.conditions.audio_for(i), self.rt.conditions.prompt, sigma=sigma, noise_key=key,
-                        stream=self.stream)
+                        stream=self.stream, arena_order=True)
 
     eager = False  # force eager launches (per-kernel timing passes)
 

@@ -205,8 +205,10 @@ class Forward:
     # ------------------------------------------------------------ inputs ----
     def write_inputs(self, block_index: int, t_index: int, steps: int, segments, cur_row: int,
                      sink_pos: int, dt: float, audio, prompt, sigma: float = 0.0, noise_key: int = 0,
-                     stream=None, sink_row: int = 0) -> None:
+                     stream=None, sink_row: int = 0, arena_order: bool = False) -> None:
         """Stage the per-call descriptor and conditioning inputs (one H2D copy).
+        ``arena_order``: let the tcgen05 attention walk the view in arena-row
+        order (engines with block-determined ring slots; lp_block_desc).
 
         ``segments``: list of (row, length, src_row) for the cache view,
         oldest first (the sink and the current block are added here)."""
@@ -217,6 +219,7 @@ class Forward:
         if len(segs) > L.MAX_SEG:
             raise ValueError(f"cache view too long for the device descriptor ({len(segs) - 2} > {L.MAX_SEG - 2})")
         d.n_seg = len(segs)
+        d.arena_order = int(bool(arena_order))
         d.cur_row = cur_row
         d.n_tokens = self.n_tokens
         for s, (r, n, src) in enumerate(segs):

@@ -20,8 +20,9 @@ def upload_desc(desc: L.BlockDesc, device="cuda:0") -> torch.Tensor:
     return torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(device)
 
 
-def make_desc(block_index, segs, cur_row, n_tokens, t_dim, sink_pos=None, base=10000.0, dt=-0.25):
+def make_desc(block_index, segs, cur_row, n_tokens, t_dim, sink_pos=None, base=10000.0, dt=-0.25, arena_order=0):
     d = L.BlockDesc()
+    d.arena_order = arena_order
     d.block_index = block_index
     d.sink_pos = block_index + 1 if sink_pos is None else sink_pos
     d.n_seg = len(segs)

@@ -86,11 +86,12 @@ def test_flash_attention_matches_reference(case):
     assert torch.equal(tc, tc2)
 
 
-def test_segments_are_visited_in_arena_order():
-    # softmax(QK^T)V does not depend on key order; the tcgen05 kernel walks
-    # the segments in arena-row order and merges adjacent ones, so the
-    # descriptor's logical order changes nothing (bitwise), and moving the
-    # same keys to other rows changes only the rounding
+def test_segment_order_modes():
+    # softmax(QK^T)V does not depend on key order.  arena_order = 1 (the
+    # engines): segments walked in arena-row order, adjacent ones merged, so
+    # the descriptor's logical order changes nothing (bitwise) and a merged
+    # range equals its parts.  arena_order = 0 (the drop-in): logical order,
+    # so moving the same keys to other rows changes nothing (bitwise).
     heads, n_q, d = 2, 256, 256
     g = torch.Generator(device=DEV).manual_seed(9)
     ka = torch.randn((1500, d), generator=g, device=DEV).to(torch.bfloat16)
@@ -99,18 +100,24 @@ def test_segments_are_visited_in_arena_order():
     scale = 0.0883883461356163
     sa = [(0, 64), (300, 256), (556, 144), (700, 256), (1200, n_q)]
     sb = [(0, 64), (700, 256), (556, 144), (300, 256), (1200, n_q)]
-    a = _run("lp_attention", q, ka, va, make_desc(3, sa, 1200, n_q, 128), heads, scale, 976)
-    b = _run("lp_attention", q, ka, va, make_desc(3, sb, 1200, n_q, 128), heads, scale, 976)
-    assert torch.equal(a, b)
-    # one merged range [300, 956) == the three adjacent segments
     sc = [(0, 64), (300, 656), (1200, n_q)]
-    c = _run("lp_attention", q, ka, va, make_desc(3, sc, 1200, n_q, 128), heads, scale, 976)
-    assert torch.equal(a, c)
+
+    def run(ka_, va_, segs, order):
+        return _run("lp_attention", q, ka_, va_, make_desc(3, segs, 1200, n_q, 128, arena_order=order), heads,
+                    scale, 976)
+
+    a = run(ka, va, sa, 1)
+    assert torch.equal(a, run(ka, va, sb, 1))
+    assert torch.equal(a, run(ka, va, sc, 1))
+    # logical order: swap which rows hold blocks 1 and 3 and list them so the
+    # logical key order is unchanged -> bitwise equal
     kb, vb = ka.clone(), va.clone()
     kb[300:556], kb[700:956] = ka[700:956], ka[300:556]
     vb[300:556], vb[700:956] = va[700:956], va[300:556]
-    e = _run("lp_attention", q, kb, vb, make_desc(3, sa, 1200, n_q, 128), heads, scale, 976)
-    assert rel_l2(e.float().cpu(), a.float().cpu()) < 1e-2
+    l0 = run(ka, va, sa, 0)
+    assert torch.equal(l0, run(kb, vb, sb, 0))
+    # the two modes differ only by rounding
+    assert rel_l2(l0.float().cpu(), a.float().cpu()) < 1e-2
 
 
 @pytest.mark.parametrize("heads", [40, 12])

@@ -236,3 +236,36 @@ def test_drop_in_denoiser_wan_bf16_matches_engine():
     fast = lp.run_sequential(cfg)
     for a, b in zip(outs, fast.blocks):
         assert rel_l2(a.values, b.values) < 1e-3
+
+
+def test_drop_in_denoiser_is_reentrant_across_threads():
+    # the reference TPP engine calls ONE denoiser object from T threads at
+    # once (engine.py:431-463): concurrent calls for different t_index must
+    # give the same bits as the same calls made one after another
+    import threading
+
+    _, pp = _profiles()
+    cfg = lp.EngineConfig(mode="sequential", profile=pp, precision="bf16", steps=4, blocks=2, cache_capacity=2)
+    rt = lp.build_runtime(cfg)
+    dn = lp.B200Denoiser(rt.weights, rt.schedule, precision="bf16", profile=pp)
+    cond = lp.BlockCond(rt.conditions.audio_for(0), rt.conditions.prompt)
+    sink = rt.conditions.reference.copy()
+    xs = {j: lp.noise_block(cfg, j) for j in range(1, 5)}
+    serial = {j: dn.denoise_block(xs[j], j, (), cond, sink, 1).velocity for j in range(1, 5)}
+    got, errs = {}, []
+
+    def work(j):
+        try:
+            for _ in range(3):
+                got[j] = dn.denoise_block(xs[j], j, (), cond, sink, 1).velocity
+        except BaseException as exc:  # noqa: BLE001
+            errs.append(exc)
+
+    th = [threading.Thread(target=work, args=(j,)) for j in range(1, 5)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for j in range(1, 5):
+        assert got[j].tobytes() == serial[j].tobytes()
