@@ -269,3 +269,15 @@ def test_drop_in_denoiser_is_reentrant_across_threads():
     assert not errs, errs
     for j in range(1, 5):
         assert got[j].tobytes() == serial[j].tobytes()
+
+
+@pytest.mark.parametrize("capacity", [1, 2])
+def test_wan_tpp_long_stream_device_noise_equals_sequential(capacity):
+    # 14 blocks through rings of L+1 = 5 slots (several wrap-arounds), device
+    # Philox history noise and random device weights, link FIFO capacity 1/2
+    _, pp = _profiles()
+    kw = dict(profile=pp, precision="bf16", steps=4, cache_capacity=4, blocks=14, device_inputs=True,
+              history_sigma=0.1, history_mode="scaled")
+    seq = lp.run(lp.EngineConfig(mode="sequential", **kw))
+    tpp = lp.run(lp.EngineConfig(mode="tpp", link_capacity=capacity, **kw))
+    assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(seq.blocks, tpp.blocks))
