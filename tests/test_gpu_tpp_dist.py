@@ -60,3 +60,21 @@ def test_ipc_tpp_bf16_wan_history_noise_equals_sequential(tmp_path):
     got = np.load(f"{out}.0.npy")
     seq = lp.run_sequential(lp.EngineConfig(mode="sequential", precision="bf16", profile=wan_small(), **kw))
     assert got.tobytes() == np.stack([b.values for b in seq.blocks]).tobytes()
+
+
+def test_ipc_tpp_decode_rank_runs_patch_codec(tmp_path):
+    # 2 DiT ranks + 1 decode rank on the Wan profile with the patch codec: the
+    # decode rank decodes every block on its GPU and runs the AAS round trip;
+    # latents and frames equal the single-process sequential run bitwise
+    import hashlib
+
+    kw = dict(steps=4, blocks=3, cache_capacity=2, patch_codec=1, pixel_scale=4, upsample=2)
+    out = tmp_path / "res"
+    launch(3, "gpu", out, dict(kw, precision="bf16", profile="wan_small", link_timeout_s=60.0, decode_gpu=1),
+           timeout=600)
+    got = np.load(f"{out}.0.npy")
+    rec = json.load(open(f"{out}.0"))
+    seq = lp.run_sequential(lp.EngineConfig(mode="sequential", precision="bf16", profile=wan_small(),
+                                            **dict(kw, patch_codec=True)))
+    assert got.tobytes() == np.stack([b.values for b in seq.blocks]).tobytes()
+    assert rec["frames_sha256"] == hashlib.sha256(seq.frames.astype("<f4").tobytes()).hexdigest()
