@@ -281,3 +281,14 @@ def test_wan_tpp_long_stream_device_noise_equals_sequential(capacity):
     seq = lp.run(lp.EngineConfig(mode="sequential", **kw))
     tpp = lp.run(lp.EngineConfig(mode="tpp", link_capacity=capacity, **kw))
     assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(seq.blocks, tpp.blocks))
+
+
+def test_graph_replay_equals_eager_launches(monkeypatch):
+    # the captured per-stage graphs (incl. the fork/join tail branch of a
+    # forced pair split) replay exactly the eager launch sequence
+    monkeypatch.setenv("LP_PAIR_SPLIT_ALL", "1")
+    _, pp = _profiles(layers=2, heads=2, ffn=512, h=16, w=24)
+    kw = dict(profile=pp, precision="bf16", steps=3, blocks=4, cache_capacity=2)
+    g = lp.run(lp.EngineConfig(mode="sequential", **kw))
+    e = lp.run(lp.EngineConfig(mode="sequential", use_graphs=False, **kw))
+    assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(g.blocks, e.blocks))
