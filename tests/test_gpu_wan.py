@@ -292,3 +292,30 @@ def test_graph_replay_equals_eager_launches(monkeypatch):
     g = lp.run(lp.EngineConfig(mode="sequential", **kw))
     e = lp.run(lp.EngineConfig(mode="sequential", use_graphs=False, **kw))
     assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(g.blocks, e.blocks))
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", TOL_FP32), ("bf16", TOL_BF16)])
+def test_drop_in_single_call_wan_matches_oracle(precision, tol):
+    # one denoise_block call with a 2-entry view (reference-shaped entries
+    # from the oracle), Wan profile, vs the oracle's dit_forward
+    po, pp = _profiles()
+    cfg = lp.EngineConfig(mode="sequential", profile=pp, precision=precision, steps=4, blocks=3, cache_capacity=2)
+    rt = lp.build_runtime(cfg)
+    wo = O.build_weights(cfg.weight_seed, po)
+    dn = lp.B200Denoiser(rt.weights, rt.schedule, precision=precision, profile=pp)
+    audio, prompt, ref_sink = rt.conditions.audio_for(2), rt.conditions.prompt, rt.conditions.reference
+    # build a 2-entry view for step j = 3 with the oracle, then hand the same
+    # K/V to the drop-in as host KvEntry objects
+    view_o, view_l = [], []
+    for i in range(2):
+        x = lp.noise_block(cfg, i).values
+        _, ent = O.dit_forward(po, wo, 4, x, i, 3, view_o, rt.conditions.audio_for(i), prompt, ref_sink, i + 1,
+                               mm=O.mm_f64, max_entries=2)
+        view_o.append(ent)
+        view_l.append(lp.KvEntry(tuple(np.asarray(k, np.float32) for k in ent.keys),
+                                 tuple(np.asarray(v, np.float32) for v in ent.values), i, 3, i))
+    x = lp.noise_block(cfg, 2)
+    vel_o, _ = O.dit_forward(po, wo, 4, x.values, 2, 3, view_o, audio, prompt, ref_sink, 3, mm=O.mm_f64,
+                             max_entries=2)
+    out = dn.denoise_block(x, 3, tuple(view_l), lp.BlockCond(audio, prompt), ref_sink, 3, max_entries=2)
+    assert rel_l2(out.velocity, vel_o) < tol
