@@ -78,3 +78,22 @@ def test_ipc_tpp_decode_rank_runs_patch_codec(tmp_path):
                                             **dict(kw, patch_codec=True)))
     assert got.tobytes() == np.stack([b.values for b in seq.blocks]).tobytes()
     assert rec["frames_sha256"] == hashlib.sha256(seq.frames.astype("<f4").tobytes()).hexdigest()
+
+
+def test_ipc_two_pipelines_of_four_ranks(tmp_path):
+    # the 8-GPU layout (two independent 4-stage pipelines, different noise
+    # seeds) with 8 ranks sharing one GPU: each pipeline equals the
+    # sequential run with its own seed, bitwise
+    import dataclasses
+
+    from paper_2512_04677_b200 import tpp_dist
+
+    kw = dict(steps=4, blocks=3, cache_capacity=2)
+    out = tmp_path / "res"
+    launch(8, "gpu", out, dict(kw, precision="bf16", profile="wan_small", link_timeout_s=90.0), timeout=900)
+    for pipe in (0, 1):
+        got = np.load(f"{out}.{pipe}.npy")
+        cfg = lp.EngineConfig(mode="sequential", precision="bf16", profile=wan_small(), **kw)
+        cfg = dataclasses.replace(cfg, noise_seed=tpp_dist.pipe_noise_seed(cfg, pipe))
+        seq = lp.run_sequential(cfg)
+        assert got.tobytes() == np.stack([b.values for b in seq.blocks]).tobytes(), pipe
