@@ -319,3 +319,13 @@ def test_drop_in_single_call_wan_matches_oracle(precision, tol):
                              max_entries=2)
     out = dn.denoise_block(x, 3, tuple(view_l), lp.BlockCond(audio, prompt), ref_sink, 3, max_entries=2)
     assert rel_l2(out.velocity, vel_o) < tol
+
+
+@pytest.mark.parametrize("delta,cap", [(3, 1), (1, 4)])
+def test_wan_sink_delta_and_window_vs_oracle(delta, cap):
+    # RSFM sink position i + delta (kvcache.py:86-90) and window sizes L = 1, 4
+    po, pp = _profiles()
+    kw = dict(steps=2, blocks=6, cache_capacity=cap, sink_delta=delta)
+    ref = _oracle(po, **kw)
+    res = _engine(pp, "bf16", **kw)
+    assert max(rel_l2(b.values, r) for b, r in zip(res.blocks, ref)) < TOL_BF16
