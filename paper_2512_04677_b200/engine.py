@@ -578,12 +578,23 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
         abort_evt.set()
         abort.fill_(1)
 
+    # every device buffer the workers touch exists before the first thread
+    # starts: an allocation while another stage's link kernel spins may wait
+    # on the device
+    statuses = [torch.zeros(1, dtype=torch.int32, device=f"cuda:{st.device}") for st in stages]
+    dec_buf = torch.zeros((cfg.frames_per_block, prof.latent_dim), dtype=torch.float32, device=f"cuda:{last_dev}")
+    dec_status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{last_dev}")
+    dec_stream = torch.cuda.Stream(last_dev)
+    for st in stages:  # the reference sink (its projection scratch is allocated here, not mid-stream)
+        st.set_sink(rt.conditions.reference.copy())
+    for d in sorted(set(devs)):
+        torch.cuda.synchronize(d)
+
     def stage_worker(k: int) -> None:
         st = stages[k - 1]
         sink = SinkSlot(rt.conditions.reference.copy(), cfg.sink_delta)
-        status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{st.device}")
+        status = statuses[k - 1]
         try:
-            st.set_sink(sink.content)
             for i in range(cfg.blocks):
                 if i == 1:
                     while True:
@@ -610,9 +621,7 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
 
     def decode_worker() -> None:
         dev = last_dev
-        stream = torch.cuda.Stream(dev)
-        buf = torch.zeros((cfg.frames_per_block, prof.latent_dim), dtype=torch.float32, device=f"cuda:{dev}")
-        status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{dev}")
+        stream, buf, status = dec_stream, dec_buf, dec_status
         try:
             for i in range(cfg.blocks):
                 with torch.cuda.device(dev), torch.cuda.stream(stream):
