@@ -587,6 +587,9 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
     dec_stream = torch.cuda.Stream(last_dev)
     for st in stages:  # the reference sink (its projection scratch is allocated here, not mid-stream)
         st.set_sink(rt.conditions.reference.copy())
+    dc = _dcodec(rt, last_dev)  # the decode stage's device codec (map uploads) likewise
+    if dc is not None:  # and one decode + AAS encode, so their buffers come from the allocator's cache later
+        dc.encode(dc.decode(LatentBlock(np.zeros((cfg.frames_per_block, dc.latent_dim), F32), 0))[0])
     for d in sorted(set(devs)):
         torch.cuda.synchronize(d)
 
