@@ -343,3 +343,22 @@ def test_14b_shape_tpp_bitwise_equals_sequential():
     tpp = [b.values for b in lp.run(lp.EngineConfig(mode="tpp", **kw)).blocks]
     assert all(a.tobytes() == b.tobytes() for a, b in zip(seq, tpp))
     assert all(np.isfinite(a).all() for a in seq)
+
+
+def test_streaming_pipeline_with_parity_noise_matches_run_sequential():
+    # the serving API with the reference's host-drawn corruption (fixed
+    # upload buffers) gives the same bits as the sequential engine
+    _, pp = _profiles()
+    cfg = lp.EngineConfig(mode="sequential", profile=pp, precision="bf16", steps=3, blocks=4, cache_capacity=2,
+                          history_sigma=0.2)
+    rt = lp.build_runtime(cfg)
+    ref = lp.run_sequential(cfg, rt)
+    pipe = lp.StreamingPipeline(cfg, lp.build_runtime(cfg))
+    for i in range(4):
+        noise = torch.from_numpy(lp.noise_block(cfg, i).values).pin_memory()
+        out = torch.empty_like(noise).pin_memory()
+        x = pipe.submit(i, noise, out=out)
+        torch.cuda.synchronize()
+        if i == 0:
+            pipe.aas(x)
+        assert out.numpy().tobytes() == ref.blocks[i].values.tobytes(), i
