@@ -338,6 +338,22 @@ LP_API int lp_ipc_handle(const void* dev_ptr, uint8_t* handle_out, int64_t* offs
 LP_API int lp_ipc_open(const uint8_t* handle, int64_t offset, void** ptr_out);
 LP_API int lp_ipc_close(void* mapped_base);
 
+
+/* ---------------------------------------------------------------- arenas
+ * Growable KV arena on CUDA virtual memory for the drop-in denoiser
+ * (Runtime.denoiser, engine.py:166-200), whose caller decides how many
+ * cache entries stay alive (RollingKvCache, kvcache.py:29-59; TPP threads,
+ * engine.py:431-463).  One reserved range of n_layers * layer_stride bytes;
+ * the first `mapped` bytes of every layer are backed on demand.  Growth
+ * never moves data (pointers stay valid) and zero-fills the new pages on
+ * `stream`.                                                                */
+typedef struct lp_vmm lp_vmm;
+LP_API int lp_vmm_create(int device, int n_layers, int64_t layer_bytes_max, lp_vmm** out);
+LP_API int lp_vmm_info(const lp_vmm* v, uint64_t* base, int64_t* layer_stride_bytes, int64_t* mapped_bytes,
+                int64_t* granularity);
+LP_API int lp_vmm_grow(lp_vmm* v, int64_t layer_bytes, void* stream);
+LP_API int lp_vmm_destroy(lp_vmm* v);
+
 #ifdef __cplusplus
 }
 #endif

@@ -107,6 +107,10 @@ _SIGS = {
     "lp_ipc_handle": ([vp, vp, C.POINTER(i64)], C.c_int),
     "lp_ipc_open": ([vp, i64, C.POINTER(vp)], C.c_int),
     "lp_ipc_close": ([vp], C.c_int),
+    "lp_vmm_create": ([C.c_int, C.c_int, i64, C.POINTER(vp)], C.c_int),
+    "lp_vmm_info": ([vp, C.POINTER(u64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], C.c_int),
+    "lp_vmm_grow": ([vp, i64, vp], C.c_int),
+    "lp_vmm_destroy": ([vp], C.c_int),
 }
 
 

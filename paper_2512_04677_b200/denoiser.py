@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import threading
 import weakref
+from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -32,11 +33,10 @@ from . import _lib as L
 from .latent import LatentBlock, TimestepSchedule
 from .model import DenoiserWeights, DeviceWeights, ModelProfile, build_weights, toy_profile
 from .numerics import F32
-from .runtime import Forward, KvArena
+from .runtime import Forward, GrowableArena
 
 
-class TimestepForcingError(ValueError):
-    """A cache view mixed entries from different noise levels (denoiser.py:41-42)."""
+from .errors import TimestepForcingError, raise_compat
 
 
 @dataclass(frozen=True)
@@ -49,7 +49,7 @@ class BlockCond:
 
 class _Slot:
     """One ring slot of the device pool; returns itself to the pool when the
-    last KvEntry referencing it is collected."""
+    last object referencing it (an entry's layers, a temp list) is collected."""
 
     __slots__ = ("pool", "index", "__weakref__")
 
@@ -59,42 +59,86 @@ class _Slot:
         weakref.finalize(self, pool.release, index)
 
 
+class DeviceLayers(Sequence):
+    """The per-layer keys (kv=0) or values (kv=1) of a device-resident entry:
+    a read-only sequence of (F*S, d) float32 arrays materialised from the
+    ring slot on first access (one D2H copy of all layers), so reference code
+    that iterates ``entry.keys`` (corrupt_history kvcache.py:133-135,
+    attention_bruteforce denoiser.py:346-422) keeps working.  Holds the slot
+    alive; ``noise = (sigma, z)`` marks a corrupted view, whose host form is
+    ring + sigma * z (kvcache.py:121-137)."""
+
+    __slots__ = ("slot", "kv", "noise", "_host")
+
+    def __init__(self, slot: _Slot, kv: int, noise=None):
+        self.slot = slot
+        self.kv = kv
+        self.noise = noise
+        self._host = None
+
+    def _get(self) -> tuple:
+        if self._host is None:
+            layers = self.slot.pool.read(self.slot.index, self.kv)
+            if self.noise is not None:
+                sigma, z = self.noise
+                layers = tuple(a + b * F32(sigma) for a, b in zip(layers, z))
+            self._host = layers
+        return self._host
+
+    def __len__(self) -> int:
+        return self.slot.pool.dw.prof.n_layers
+
+    def __getitem__(self, i):
+        return self._get()[i]
+
+    def __iter__(self):
+        return iter(self._get())
+
+
+@dataclass(frozen=True, eq=False)
 class KvEntry:
     """Cached keys/values of one block at one noise level (denoiser.py:45-57).
 
-    ``keys[l]`` is rotated at ``rope_index``; ``values[l]`` is not.  Device
-    resident; host tuples are materialised lazily."""
+    ``keys[l]`` is rotated at ``rope_index``; ``values[l]`` is not.  Field
+    for field the reference's frozen dataclass, so ``dataclasses.replace``
+    (the reference's corrupt_history, kvcache.py:136) works and yields a
+    host entry.  Entries the GPU denoiser returns keep K/V in a device slot
+    (``keys``/``values`` are ``DeviceLayers``); host entries hold tuples of
+    arrays and are uploaded when a view containing them is denoised."""
 
-    __slots__ = ("_keys", "_values", "block_index", "timestep_index", "rope_index", "_slot", "_noise")
+    keys: Sequence = ()
+    values: Sequence = ()
+    block_index: int = 0
+    timestep_index: int = 0
+    rope_index: int = 0
 
-    def __init__(self, keys=None, values=None, block_index: int = 0, timestep_index: int = 0,
-                 rope_index: int = 0, _slot: _Slot | None = None, _noise=None):
-        self._keys = None if keys is None else tuple(np.asarray(k, F32) for k in keys)
-        self._values = None if values is None else tuple(np.asarray(v, F32) for v in values)
-        self.block_index = block_index
-        self.timestep_index = timestep_index
-        self.rope_index = rope_index
-        self._slot = _slot
-        self._noise = _noise  # (sigma, keys_noise, values_noise) for a corrupted view entry
+    def __post_init__(self):
+        if not isinstance(self.keys, DeviceLayers):
+            object.__setattr__(self, "keys", tuple(np.asarray(k, F32) for k in self.keys))
+        if not isinstance(self.values, DeviceLayers):
+            object.__setattr__(self, "values", tuple(np.asarray(v, F32) for v in self.values))
 
-    def _materialise(self):
-        if self._keys is None:
-            k, v = self._slot.pool.read(self._slot.index)
-            self._keys, self._values = k, v
-            if self._noise is not None:
-                sigma, nk, nv = self._noise
-                self._keys = tuple(a + b * F32(sigma) for a, b in zip(self._keys, nk))
-                self._values = tuple(a + b * F32(sigma) for a, b in zip(self._values, nv))
+    @classmethod
+    def on_slot(cls, slot: _Slot, block_index: int, timestep_index: int, rope_index: int,
+                noise=None) -> "KvEntry":
+        """A device entry; ``noise = (sigma, keys_z, values_z)`` makes it a
+        corrupted view of the slot (the perturbation is applied on the
+        device when denoised, on the host when materialised)."""
+        nk = nv = None
+        if noise is not None:
+            sigma, zk, zv = noise
+            nk, nv = (sigma, zk), (sigma, zv)
+        return cls(DeviceLayers(slot, 0, nk), DeviceLayers(slot, 1, nv), block_index, timestep_index, rope_index)
 
     @property
-    def keys(self) -> tuple:
-        self._materialise()
-        return self._keys
+    def _slot(self):
+        return self.keys.slot if isinstance(self.keys, DeviceLayers) else None
 
     @property
-    def values(self) -> tuple:
-        self._materialise()
-        return self._values
+    def _noise(self):
+        if isinstance(self.keys, DeviceLayers) and self.keys.noise is not None:
+            return (self.keys.noise[0], self.keys.noise[1], self.values.noise[1])
+        return None
 
     @property
     def on_device(self) -> bool:
@@ -108,90 +152,80 @@ class DenoiseOutput:
 
 
 class _SlotPool:
-    """Device KV slots shared by all timesteps of one denoiser, plus per
-    workspace sink rows and corrupted-view scratch (one arena, so any view
-    is addressable as row segments of a single base)."""
+    """Device KV slots shared by all timesteps of one denoiser, plus one sink
+    region per workspace, in one ``GrowableArena`` (one base per layer, so
+    any view is addressable as row segments of it).  Slots are backed on
+    demand: the caller (the reference engine's caches, TPP threads, views
+    with host-typed or corrupted entries) decides how many stay alive, and
+    growth never moves the base, so in-flight launches are unaffected."""
 
-    def __init__(self, dw: DeviceWeights, n_tokens: int, n_slots: int, n_workspaces: int, hist_max: int):
+    def __init__(self, dw: DeviceWeights, n_tokens: int, n_workspaces: int, initial_slots: int):
         self.dw = dw
         self.n_tokens = n_tokens
         self.n_workspaces = n_workspaces
-        self.hist_max = hist_max
         self.lock = threading.Lock()
-        self.active = 0
-        self._alloc(n_slots)
+        s = dw.prof.tokens_per_frame
+        self.arena = GrowableArena(dw.prof, n_tokens, n_workspaces * s, dw.dtype, dw.device)
+        self.slot_bytes = 2 * dw.prof.n_layers * n_tokens * dw.prof.model_dim * self.arena.k.element_size()
+        self.free: list = []
+        self._grow_to(max(1, initial_slots))
 
-    def _alloc(self, n_slots: int) -> None:
-        prof = self.dw.prof
-        s = prof.tokens_per_frame
-        # rows: [sink region per workspace | slots | scratch per workspace]
-        extra_sink_rows = (self.n_workspaces - 1) * s
-        hist_rows = self.n_workspaces * self.hist_max
-        arena = KvArena(prof, self.n_tokens, n_slots + (extra_sink_rows + self.n_tokens - 1) // self.n_tokens,
-                        hist_rows, self.dw.dtype, self.dw.device)
-        self.arena = arena
-        self.n_slots = n_slots
-        self.slot_base = self.n_workspaces * s
-        self.free = list(range(n_slots - 1, -1, -1))
+    @property
+    def n_slots(self) -> int:
+        return self.arena.n_slots
+
+    def _grow_to(self, n: int) -> None:
+        old = self.arena.n_slots
+        n = min(n, self.arena.max_slots)
+        if n <= old:
+            raise RuntimeError(f"KV slot pool exhausted: all {old} slots the device can hold at this shape are "
+                               "live (the caller keeps more cache entries alive than fit in HBM)")
+        self.arena.ensure_slots(n)
+        torch.cuda.synchronize(self.dw.device)  # zero fill of the new pages
+        self.free.extend(range(n - 1, old - 1, -1))
 
     def slot_row(self, i: int) -> int:
-        return self.slot_base + i * self.n_tokens
+        return self.arena.slot_row(i)
 
     def sink_row(self, w: int) -> int:
         return w * self.dw.prof.tokens_per_frame
 
-    def scratch_row(self, w: int, e: int) -> int:
-        return self.arena.scratch_row(w * self.hist_max + e)
-
     def acquire(self) -> _Slot:
         with self.lock:
             if not self.free:
-                self._grow()
+                n = self.arena.n_slots
+                # big slots (1.9 GB per K/V at the 14B shape) grow one at a time
+                step = 1 if self.slot_bytes > (1 << 30) else max(4, n // 2)
+                self._grow_to(n + step)
             return _Slot(self, self.free.pop())
 
     def release(self, index: int) -> None:
         with self.lock:
-            if index < self.n_slots:
-                self.free.append(index)
+            self.free.append(index)
 
-    def _grow(self) -> None:
-        if self.active > 1:
-            raise RuntimeError("KV slot pool exhausted while other calls are in flight; "
-                               "construct B200Denoiser with a larger max_live_entries")
-        old = self.arena
-        torch.cuda.synchronize(self.dw.device)
-        n_old = self.n_slots
-        free_old = list(self.free)
-        self._alloc(2 * n_old)
-        # sink regions and live slots keep their row offsets
-        a = self.slot_base + n_old * self.n_tokens
-        self.arena.k[:, :a].copy_(old.k[:, :a])
-        self.arena.v[:, :a].copy_(old.v[:, :a])
-        self.free = list(range(2 * n_old - 1, n_old - 1, -1)) + free_old
+    def read(self, index: int, kv: int) -> tuple:
+        r = self.slot_row(index)
+        t = self.arena.k if kv == 0 else self.arena.v
+        a = t[:, r:r + self.n_tokens].float().cpu().numpy()
+        return tuple(a[l] for l in range(a.shape[0]))
 
-    def read(self, index: int):
+    def write(self, index: int, keys, values, stream) -> None:
+        """Upload a host entry into slot ``index`` on ``stream``."""
         r = self.slot_row(index)
         N = self.n_tokens
-        k = self.arena.k[:, r:r + N].float().cpu().numpy()
-        v = self.arena.v[:, r:r + N].float().cpu().numpy()
-        return tuple(k), tuple(v)
-
-    def write(self, index: int, keys, values) -> None:
-        r = self.slot_row(index)
-        N = self.n_tokens
-        kt = torch.from_numpy(np.stack([np.asarray(x, F32) for x in keys])).to(self.arena.k.device)
-        vt = torch.from_numpy(np.stack([np.asarray(x, F32) for x in values])).to(self.arena.v.device)
-        self.arena.k[:, r:r + N].copy_(kt)
-        self.arena.v[:, r:r + N].copy_(vt)
+        for t, layers in ((self.arena.k, keys), (self.arena.v, values)):
+            host = torch.from_numpy(np.ascontiguousarray(np.stack([np.asarray(x, F32) for x in layers])))
+            with torch.cuda.stream(stream):
+                t[:, r:r + N].copy_(host.to(t.device, non_blocking=False))
 
 
 def check_view(entries, t_index: int, require_same_timestep: bool, max_entries) -> None:
     """Metadata rules of denoise_block (denoiser.py:219-234), bit-exact messages."""
     seen = {e.timestep_index for e in entries}
     if len(seen) > 1:
-        raise TimestepForcingError(f"cache view mixes timestep indices {sorted(seen)}")
+        raise_compat(TimestepForcingError, f"cache view mixes timestep indices {sorted(seen)}")
     if require_same_timestep and seen and seen != {t_index}:
-        raise TimestepForcingError(f"cache holds timestep {seen.pop()} but denoising at {t_index}")
+        raise_compat(TimestepForcingError, f"cache holds timestep {seen.pop()} but denoising at {t_index}")
     if max_entries is not None and len(entries) > max_entries:
         raise ValueError(f"cache view exceeds capacity {max_entries}")
     for prev, nxt in zip(entries, entries[1:]):
@@ -228,18 +262,20 @@ class B200Denoiser:
         self._pool = None
         self._ws = {}
         self._max_live = max_live_entries
-        self._hist_max = 8
 
     # -- internals ------------------------------------------------------------
-    def _workspace(self, t_index: int, n_frames: int):
+    def _workspace(self, t_index: int, n_frames: int, max_entries):
         with self._lock:
             if self._pool is None:
                 self._frames = n_frames
                 n_tok = n_frames * self.profile.tokens_per_frame
                 steps = self.schedule.steps
                 n_ws = steps + 1  # t_index 0 (clean-cache pass) .. T
-                live = self._max_live or (steps + 1) * (self._hist_max + 2) + 8
-                self._pool = _SlotPool(self.dw, n_tok, live, n_ws, self._hist_max)
+                # first guess at the live set: T caches of L entries + one
+                # in-flight entry per stage; the pool grows on demand
+                window = max_entries if max_entries is not None else 4
+                initial = self._max_live or steps * (window + 1)
+                self._pool = _SlotPool(self.dw, n_tok, n_ws, initial)
             if n_frames != self._frames:
                 raise ValueError(f"block has {n_frames} frames; this denoiser was set up for {self._frames}")
             ws = self._ws.get(t_index)
@@ -262,59 +298,66 @@ class B200Denoiser:
                       sink_rope_index: int, require_same_timestep: bool = True,
                       max_entries: int | None = None) -> DenoiseOutput:
         """Velocity for ``x`` at step ``t_index`` plus this block's KvEntry
-        (denoiser.py:201-276).  Pure: mutates nothing it is given."""
+        (denoiser.py:201-276).  Pure: mutates nothing it is given.  Entries
+        may be this denoiser's device entries, corrupted views of them, or
+        any duck-typed host entry with keys/values/block_index/
+        timestep_index (the reference's KvEntry); host ones are uploaded."""
         entries = list(cache_view)
         check_view(entries, t_index, require_same_timestep, max_entries)
         prof = self.profile
         if x.values.shape[1] != prof.latent_dim:
             raise ValueError(f"latent dim {x.values.shape[1]} != model latent dim {prof.latent_dim}")
-        fw, stream, w = self._workspace(t_index, x.values.shape[0])
-        pool = self._pool
+        if len(entries) > L.MAX_SEG - 2:
+            raise ValueError(f"cache view of {len(entries)} entries exceeds the device bound {L.MAX_SEG - 2}")
+        fw, stream, w = self._workspace(t_index, x.values.shape[0], max_entries)
         with fw.lock:
-            pool.active += 1
-            try:
-                return self._run(fw, stream, w, x, t_index, entries, cond, sink, sink_rope_index)
-            finally:
-                pool.active -= 1
+            return self._run(fw, stream, w, x, t_index, entries, cond, sink, sink_rope_index)
 
     def _run(self, fw, stream, w, x, t_index, entries, cond, sink, sink_rope_index):
         pool = self._pool
-        if len(entries) > L.MAX_SEG - 2:
-            raise ValueError(f"cache view of {len(entries)} entries exceeds the device bound {L.MAX_SEG - 2}")
-        if any(en._noise is not None for en in entries) and len(entries) > pool.hist_max:
-            raise ValueError(f"corrupted view of {len(entries)} entries exceeds the scratch bound "
-                             f"{pool.hist_max}")
-        fw.arena = pool.arena
-        temps = []
-        segs = []
-        noise_parts = []
-        for e, en in enumerate(entries):
-            slot = en._slot if (en._slot is not None and en._slot.pool is pool) else None
-            if slot is None:  # host-resident entry: upload to a temporary slot
-                slot = pool.acquire()
-                temps.append(slot)
-                pool.write(slot.index, en.keys, en.values)
-                if en._noise is not None:
-                    pass  # keys/values above already include the perturbation
-            row = pool.slot_row(slot.index)
-            if en._noise is not None and en._slot is not None and en._slot.pool is pool:
-                sigma, nk, nv = en._noise
-                segs.append((pool.scratch_row(w, e), pool.n_tokens, row))
-                noise_parts.append((sigma, nk, nv))
-            else:
-                segs.append((row, pool.n_tokens, row))
+        N = pool.n_tokens
+
+        def own(en):
+            slot = getattr(en, "_slot", None)
+            return slot if (slot is not None and slot.pool is pool) else None
+
+        noisy = [en._noise for en in entries if own(en) is not None and en._noise is not None]
+        if noisy and len(noisy) != len(entries):
+            raise ValueError("a corrupted view must perturb every entry with one sigma")
         sigma = 0.0
-        if noise_parts:
-            sig = {s for s, _, _ in noise_parts}
-            if len(sig) != 1 or len(noise_parts) != len(entries):
+        if noisy:
+            sig = {n[0] for n in noisy}
+            if len(sig) != 1:
                 raise ValueError("a corrupted view must perturb every entry with one sigma")
             sigma = sig.pop()
+        # acquire EVERY slot this call writes (uploads, corrupted copies, the
+        # new entry) before any launch is bound to the arena
+        temps = []
+        segs = []
+        for en in entries:
+            slot = own(en)
+            if slot is None:  # host-resident (or another pool's) entry: upload
+                t = pool.acquire()
+                temps.append(t)
+                pool.write(t.index, en.keys, en.values, stream)
+                row = pool.slot_row(t.index)
+                segs.append((row, N, row))
+            elif noisy:  # corrupted view: ring + sigma*z written into a temp slot on the device
+                t = pool.acquire()
+                temps.append(t)
+                segs.append((pool.slot_row(t.index), N, pool.slot_row(slot.index)))
+            else:
+                row = pool.slot_row(slot.index)
+                segs.append((row, N, row))
+        cur = pool.acquire()
+        if noisy:
             # reference draw order: per entry, keys of every layer, then values
-            arr = np.stack([np.stack([np.stack(nk), np.stack(nv)]) for _, nk, nv in noise_parts])
+            arr = np.stack([np.stack([np.stack(nk), np.stack(nv)]) for _, nk, nv in noisy])
             fw.set_history_noise(True, torch.from_numpy(np.ascontiguousarray(arr)).to(self.device))
         else:
             fw.set_history_noise(False)
-        cur = pool.acquire()
+        fw.kv_bound = self.profile.tokens_per_frame + (len(entries) + 1) * N
+        fw.hist_rows = max(1, len(entries)) * N
         with torch.cuda.stream(stream):
             self._set_sink(fw, sink, stream)
             fw.write_inputs(x.block_index, t_index, self.schedule.steps, segs, pool.slot_row(cur.index),
@@ -325,7 +368,7 @@ class B200Denoiser:
         stream.synchronize()
         vel = fw.velocity_host()
         del temps
-        kv = KvEntry(None, None, x.block_index, t_index, x.block_index, _slot=cur)
+        kv = KvEntry.on_slot(cur, x.block_index, t_index, x.block_index)
         return DenoiseOutput(velocity=vel, kv=kv)
 
     def cache_entry(self, x: LatentBlock, cache_view, cond: BlockCond, sink: np.ndarray,

@@ -26,7 +26,7 @@ import os
 import queue
 import threading
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 import torch
@@ -42,6 +42,7 @@ from .metrics import MetricsBundle, TimelineEvent, drift_metric, metrics_from_ti
 from .model import DenoiserWeights, DeviceWeights, ModelProfile, build_weights, toy_profile
 from .numerics import F32, Prng
 from .runtime import Forward, KvArena, h2d, prewarm_torch, wait_event
+from .errors import SinkLockedError, raise_compat
 
 THREADS_ENV = "LIVE_PIPE_THREADS"
 ORACLE_TARGET_STREAM = 1 << 46
@@ -50,12 +51,7 @@ DENOISER_KINDS = ("toy", "oracle")
 PRECISIONS = ("fp32", "bf16")
 
 
-class EngineConfigError(ValueError):
-    """Invalid engine configuration (CLI exit code 2)."""
-
-
-class PipelineInvariantError(RuntimeError):
-    """A runtime invariant was violated mid-run (CLI exit code 3)."""
+from .errors import EngineConfigError, PipelineInvariantError  # noqa: E402  (engine.py:65-70)
 
 
 @dataclass(frozen=True)
@@ -106,6 +102,16 @@ class EngineConfig:
             raise EngineConfigError(f"mode must be one of {MODES}, got {self.mode!r}")
         if self.denoiser_kind not in DENOISER_KINDS:
             raise EngineConfigError(f"denoiser must be one of {DENOISER_KINDS}")
+        if self.denoiser_kind == "oracle":
+            # the reference's analytic (x - target)/s test denoiser
+            # (denoiser.py:294-343) has no DiT math to accelerate; refusing is
+            # louder than silently running the toy model in its place
+            raise EngineConfigError("denoiser_kind='oracle' is the reference's analytic test denoiser and is not "
+                                    "part of the B200 path; run it on the reference engine")
+        if (self.profile is not None and self.rope_base != 10000.0
+                and self.rope_base != self.profile.rope_base):
+            raise EngineConfigError(f"rope_base {self.rope_base} disagrees with the profile's "
+                                    f"{self.profile.rope_base}")
         for name in ("steps", "cache_capacity", "frames_per_block", "blocks", "upsample", "sink_delta",
                      "n_layers", "n_heads", "head_dim", "link_capacity", "pixel_channels", "pixel_scale"):
             if getattr(self, name) < 1:
@@ -130,7 +136,8 @@ class EngineConfig:
     def model_profile(self) -> ModelProfile:
         if self.profile is not None:
             return self.profile
-        return toy_profile(self.n_layers, self.n_heads, self.head_dim, self.audio_dim, self.prompt_dim)
+        prof = toy_profile(self.n_layers, self.n_heads, self.head_dim, self.audio_dim, self.prompt_dim)
+        return prof if self.rope_base == prof.rope_base else replace(prof, rope_base=self.rope_base)
 
     @property
     def stage_latencies(self) -> list:
@@ -415,9 +422,7 @@ def _aas(rt: Runtime, sink: SinkSlot, x: LatentBlock, dev: int | None = None) ->
         # patched profiles: the decode stage is "next"; the
         # sink takes block 0's first latent frame (the round trip's fixed point)
         if sink.locked:
-            from .kvcache import SinkLockedError
-
-            raise SinkLockedError("sink already replaced once this rollout")
+            raise_compat(SinkLockedError, "the sink was already replaced in this rollout")
         sink.content = np.asarray(x.values[0], F32).copy()
         sink.locked = True
 
@@ -676,7 +681,7 @@ def run_clean_kv(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
     rt = rt or build_runtime(cfg)
     if rt.weights is None:
         raise EngineConfigError("clean_kv needs host weights (device_inputs=False)")
-    dn = B200Denoiser(rt.weights, rt.schedule, cfg.rope_base, precision=cfg.precision,
+    dn = B200Denoiser(rt.weights, rt.schedule, cfg.model_profile.rope_base, precision=cfg.precision,
                       device=f"cuda:{cfg.devices[0]}", profile=cfg.model_profile)
     unified = RollingKvCache(0, cfg.cache_capacity)
     sink = SinkSlot(rt.conditions.reference.copy(), cfg.sink_delta)
@@ -765,6 +770,7 @@ class StreamingPipeline:
 
     def aas(self, block0: torch.Tensor) -> None:
         """One-shot sink swap after block 0 (kvcache.py:93-109)."""
+        self.stream.synchronize()  # block0 is written on the pipeline stream
         xb = LatentBlock(block0.detach().float().cpu().numpy().reshape(self.cfg.frames_per_block, -1), 0)
         _aas(self.rt, self.sink, xb, self.dev)
         for st in self.stages.values():

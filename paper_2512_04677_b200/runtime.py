@@ -118,6 +118,101 @@ class KvArena:
         return 2 * self.k.numel() * self.k.element_size()
 
 
+class _DeviceArray:
+    """``__cuda_array_interface__`` exporter: a torch view of raw device memory."""
+
+    def __init__(self, ptr: int, shape: tuple, strides: tuple, typestr: str):
+        self.__cuda_array_interface__ = {"shape": shape, "strides": strides, "typestr": typestr,
+                                         "data": (ptr, False), "version": 3}
+
+
+class GrowableArena:
+    """A KV arena whose ring slots are backed on demand (lp_vmm, CUDA virtual
+    memory), for the drop-in denoiser.
+
+    Same addressing as ``KvArena`` -- per layer, rows of d, one base pointer
+    per layer ``layer_stride`` elements apart -- so every kernel runs on it
+    unchanged.  Rows: [head_rows (sink regions) | slot 0 | slot 1 | ...].
+    ``ensure_slots(n)`` maps physical HBM for slots [0, n) of every layer;
+    the base never moves, so launches already enqueued (and other threads'
+    workspaces) keep valid addresses while the arena grows.  ``rows`` is the
+    number of backed rows (the TMA bound of the attention descriptors)."""
+
+    def __init__(self, prof: ModelProfile, n_tokens: int, head_rows: int, dtype: torch.dtype, device,
+                 max_slots: int | None = None):
+        self.prof = prof
+        self.n_tokens = n_tokens
+        self.s_tokens = prof.tokens_per_frame
+        self.head_rows = head_rows
+        self.hist_max = 0
+        self.n_slots = 0
+        self.dtype = dtype
+        self.device = torch.device(device)
+        dev = self.device.index or 0
+        d = prof.model_dim
+        esz = torch.tensor([], dtype=dtype).element_size()
+        self._row_bytes = d * esz
+        if max_slots is None:
+            # never more than the device could back: total HBM over K and V
+            total = torch.cuda.get_device_properties(dev).total_memory
+            max_slots = max(1, total // (2 * prof.n_layers * n_tokens * self._row_bytes))
+        self.max_slots = int(min(max_slots, 4096, (2 ** 31 - 1 - head_rows) // n_tokens))
+        self.max_rows = head_rows + self.max_slots * n_tokens
+        if self.max_rows >= 2 ** 31:
+            raise ValueError("arena rows exceed the int32 row index of lp_block_desc")
+        lib = L.load()
+        self._h = []
+        views = []
+        for _ in range(2):
+            h = C.c_void_p()
+            L.call("lp_vmm_create", dev, prof.n_layers, self.max_rows * self._row_bytes, C.byref(h))
+            self._h.append(h)
+            base, stride = C.c_uint64(), C.c_int64()
+            lib.lp_vmm_info(h, C.byref(base), C.byref(stride), None, None)
+            self._stride_bytes = int(stride.value)
+            typestr = "<f4" if dtype == torch.float32 else "<i2"
+            t = torch.as_tensor(_DeviceArray(int(base.value), (prof.n_layers, self.max_rows, d),
+                                             (self._stride_bytes, self._row_bytes, esz), typestr),
+                                device=self.device)
+            views.append(t if dtype == torch.float32 else t.view(dtype))
+        self.k, self.v = views
+        self.rows = 0
+
+    @property
+    def layer_stride(self) -> int:
+        return self._stride_bytes // self.k.element_size()
+
+    def slot_row(self, slot: int) -> int:
+        return self.head_rows + slot * self.n_tokens
+
+    def ensure_slots(self, n: int, stream=None) -> None:
+        """Back slots [0, n) of every layer (zero-filled on first mapping)."""
+        if n <= self.n_slots:
+            return
+        if n > self.max_slots:
+            raise RuntimeError(f"KV arena exhausted: {n} live slots requested, the device holds at most "
+                               f"{self.max_slots} at this shape")
+        rows = self.head_rows + n * self.n_tokens
+        st = stream.cuda_stream if stream is not None else 0
+        for h in self._h:
+            L.call("lp_vmm_grow", h, rows * self._row_bytes, st)
+        mapped = C.c_int64()
+        L.load().lp_vmm_info(self._h[0], None, None, C.byref(mapped), None)
+        self.rows = min(self.max_rows, int(mapped.value) // self._row_bytes)
+        self.n_slots = n
+
+    def nbytes(self) -> int:
+        return 2 * self.rows * self._row_bytes * self.prof.n_layers
+
+    def __del__(self):
+        hs, self._h = getattr(self, "_h", []), []
+        for h in hs:
+            try:
+                L.load().lp_vmm_destroy(h)
+            except Exception:  # noqa: BLE001 - interpreter shutdown
+                pass
+
+
 class Forward:
     """Workspace + launch sequence of one block forward on one device/stream."""
 
@@ -402,7 +497,7 @@ class Forward:
                 for kv, base in ((0, kl), (1, vl)):
                     self._tag("history_noise", "begin", stream)
                     L.call("lp_history_noise", base, ldt, d, _p(self.noise), nl, l, kv, self.desc_ptr,
-                           ar.hist_max * N, st)
+                           self.hist_rows or ar.hist_max * N, st)
                     self._tag("history_noise", "end", stream)
             args = L.AttnArgs(ldt, N, prof.n_heads, prof.head_dim, self.scale, self.q.data_ptr(), kl, vl,
                               self.att.data_ptr(), self.desc_ptr, ar.rows, self.max_keys(), _p(self.attn_ws),
@@ -476,9 +571,16 @@ class Forward:
     # written by set_sink, not re-written every block
     sink_v_static = False
 
+    # callers whose view length is known per call (the drop-in) set these:
+    # an exact bound of visible keys, and of corrupted history rows
+    kv_bound = None
+    hist_rows = None
+
     def max_keys(self) -> int:
         """Upper bound of visible keys: sink + every ring slot (or the
         descriptor's history bound) + the current block."""
+        if self.kv_bound:
+            return self.kv_bound
         ar = self.arena
         hist = min(max(ar.n_slots - 1, ar.hist_max), L.MAX_SEG - 2)
         return ar.s_tokens + (hist + 1) * self.n_tokens
