@@ -174,11 +174,23 @@ def count_nfe(result) -> int:
 @dataclass
 class Runtime:
     schedule: TimestepSchedule
-    weights: DenoiserWeights | None
+    host_weights: DenoiserWeights | None
     device_weights: dict  # device index -> DeviceWeights
     codec: ToyVideoCodec | PatchVideoCodec | None
     conditions: Conditions
     device_codecs: dict = field(default_factory=dict)  # device index -> codec.DeviceCodec
+    weight_seed: int | None = None  # host weights rebuilt on demand from (seed, profile)
+    profile: ModelProfile | None = None
+
+    @property
+    def weights(self) -> DenoiserWeights | None:
+        """Host weights (the reference container, denoiser.py:75-138).  The
+        fast path streams them to the device layer by layer and keeps no host
+        copy (9.9 B parameters at the 14B shape); they are redrawn from the
+        seed -- identical numbers -- only when a host consumer asks."""
+        if self.host_weights is None and self.weight_seed is not None:
+            self.host_weights = build_weights(self.weight_seed, profile=self.profile)
+        return self.host_weights
 
 
 def build_runtime(cfg: EngineConfig) -> Runtime:
@@ -188,12 +200,15 @@ def build_runtime(cfg: EngineConfig) -> Runtime:
     dev_ids = sorted(set(cfg.devices))
     for d in dev_ids:
         L.init_device(d)
+    seed = None
     if cfg.device_inputs:
-        w = None
         dws = {d: DeviceWeights.random(prof, cfg.precision, f"cuda:{d}", cfg.weight_seed) for d in dev_ids}
     else:
-        w = build_weights(cfg.weight_seed, profile=prof)
-        dws = {d: DeviceWeights.from_host(w, prof, cfg.precision, f"cuda:{d}") for d in dev_ids}
+        # the reference's seeded weights (build_weights, denoiser.py:100-138),
+        # drawn and uploaded one layer at a time
+        seed = cfg.weight_seed
+        dws = DeviceWeights.from_seed(seed, prof, cfg.precision, [f"cuda:{d}" for d in dev_ids])
+        dws = dict(zip(dev_ids, dws))
     codec = None
     if not prof.patched:
         codec = ToyVideoCodec(cfg.weight_seed, prof.latent_dim, cfg.pixel_dim, cfg.upsample)
@@ -201,7 +216,7 @@ def build_runtime(cfg: EngineConfig) -> Runtime:
         codec = PatchVideoCodec(cfg.weight_seed, prof.channels, prof.height, prof.width, cfg.pixel_channels,
                                 cfg.pixel_scale, cfg.upsample)
     conds = synthetic_conditions(cfg.noise_seed, cfg.blocks, prof.audio_dim, prof.prompt_dim, prof.latent_dim)
-    return Runtime(schedule, w, dws, codec, conds)
+    return Runtime(schedule, None, dws, codec, conds, weight_seed=seed, profile=prof)
 
 
 def noise_block(cfg: EngineConfig, block_index: int) -> LatentBlock:

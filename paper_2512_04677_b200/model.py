@@ -157,6 +157,41 @@ class DenoiserWeights:
         return self.n_heads * self.head_dim
 
 
+def _draw_weights(seed: int, prof: ModelProfile):
+    """The seeded draw sequence of ``build_weights``, one piece at a time:
+    yields each layer's ``LayerWeights``, then a dict of the head/conditioning
+    matrices, then (profiles with extensions) a dict of the extension
+    tensors.  Consuming it lazily keeps one layer on the host at a time."""
+    gen = Prng(seed, WEIGHT_STREAM)
+    d = prof.model_dim
+
+    def mat(rows, cols, gain=1.0):
+        return gen.normal((rows, cols)) * F32(gain / np.sqrt(rows))
+
+    for _ in range(prof.n_layers):
+        wq, wk, wv = mat(d, d), mat(d, d), mat(d, d)
+        wo = mat(d, d, 0.25)
+        w1 = mat(d, prof.ffn_dim)
+        w2 = mat(prof.ffn_dim, d, 0.25)
+        yield LayerWeights(wq, wk, wv, wo, w1, w2)
+    yield dict(w_audio=mat(prof.audio_dim, d), w_prompt=mat(prof.prompt_dim, d), w_time=mat(TIME_FEATURES, d),
+               w_vel=mat(d, prof.out_dim, 0.5))
+    if prof.patched or prof.adaln or prof.qk_norm:
+        ex = Prng(seed, WAN_EXTRA_STREAM)
+
+        def emat(rows, cols, gain):
+            return ex.normal((rows, cols)) * F32(gain / np.sqrt(rows))
+
+        w_emb = emat(prof.patch_dim, d, 1.0)
+        b_emb = ex.normal(d) * F32(0.02)
+        w_mod = emat(d, 6 * d, 0.1)
+        mod = ex.normal((prof.n_layers, 6, d)) * F32(0.1)
+        g_q = F32(1.0) + ex.normal((prof.n_layers, d)) * F32(0.05)
+        g_k = F32(1.0) + ex.normal((prof.n_layers, d)) * F32(0.05)
+        mod_head = ex.normal((2, d)) * F32(0.1)
+        yield dict(w_emb=w_emb, b_emb=b_emb, w_mod=w_mod, mod=mod, g_q=g_q, g_k=g_k, mod_head=mod_head)
+
+
 def build_weights(seed: int, n_layers: int = 2, n_heads: int = 2, head_dim: int = 8, audio_dim: int = 8,
                   prompt_dim: int = 8, profile: ModelProfile | None = None) -> DenoiserWeights:
     """Seeded host weights.  Same signature and (for the toy profile) the
@@ -165,37 +200,14 @@ def build_weights(seed: int, n_layers: int = 2, n_heads: int = 2, head_dim: int 
     w_audio, w_prompt, w_time, w_vel; N(0,1) * gain / sqrt(rows).
     Profile extension tensors are drawn from stream 1<<47."""
     prof = profile if profile is not None else toy_profile(n_layers, n_heads, head_dim, audio_dim, prompt_dim)
-    gen = Prng(seed, WEIGHT_STREAM)
-    d = prof.model_dim
-
-    def mat(rows, cols, gain=1.0):
-        return gen.normal((rows, cols)) * F32(gain / np.sqrt(rows))
-
-    layers = []
-    for _ in range(prof.n_layers):
-        wq, wk, wv = mat(d, d), mat(d, d), mat(d, d)
-        wo = mat(d, d, 0.25)
-        w1 = mat(d, prof.ffn_dim)
-        w2 = mat(prof.ffn_dim, d, 0.25)
-        layers.append(LayerWeights(wq, wk, wv, wo, w1, w2))
-    w_audio = mat(prof.audio_dim, d)
-    w_prompt = mat(prof.prompt_dim, d)
-    w_time = mat(TIME_FEATURES, d)
-    w_vel = mat(d, prof.out_dim, 0.5)
-    w = DenoiserWeights(tuple(layers), w_audio, w_prompt, w_time, w_vel, prof.n_heads, prof.head_dim, prof)
-    if prof.patched or prof.adaln or prof.qk_norm:
-        ex = Prng(seed, WAN_EXTRA_STREAM)
-
-        def emat(rows, cols, gain):
-            return ex.normal((rows, cols)) * F32(gain / np.sqrt(rows))
-
-        w.w_emb = emat(prof.patch_dim, d, 1.0)
-        w.b_emb = ex.normal(d) * F32(0.02)
-        w.w_mod = emat(d, 6 * d, 0.1)
-        w.mod = ex.normal((prof.n_layers, 6, d)) * F32(0.1)
-        w.g_q = F32(1.0) + ex.normal((prof.n_layers, d)) * F32(0.05)
-        w.g_k = F32(1.0) + ex.normal((prof.n_layers, d)) * F32(0.05)
-        w.mod_head = ex.normal((2, d)) * F32(0.1)
+    draws = _draw_weights(seed, prof)
+    layers = tuple(next(draws) for _ in range(prof.n_layers))
+    head = next(draws)
+    w = DenoiserWeights(layers, head["w_audio"], head["w_prompt"], head["w_time"], head["w_vel"], prof.n_heads,
+                        prof.head_dim, prof)
+    for extra in draws:
+        for k, v in extra.items():
+            setattr(w, k, v)
     return w
 
 
@@ -226,37 +238,80 @@ class DeviceWeights:
         self.ldt = L.LP_F32 if precision == "fp32" else L.LP_BF16
 
     # -- construction -------------------------------------------------------
+    def _f32(self, a) -> torch.Tensor:
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(self.device)
+
+    def _mm(self, a) -> torch.Tensor:
+        """A (in, out) host matrix in the kernel layout: fp32 (in, out) or bf16 W^T (out, in)."""
+        if self.precision == "fp32":
+            return self._f32(a)
+        return self._f32(np.ascontiguousarray(np.asarray(a).T)).to(torch.bfloat16)
+
+    def _qkv(self, x: LayerWeights) -> torch.Tensor:
+        if self.precision == "fp32":
+            return self._f32(np.concatenate([x.wq, x.wk, x.wv], axis=1))
+        return self._f32(np.concatenate([x.wq.T, x.wk.T, x.wv.T], axis=0)).to(torch.bfloat16)
+
+    def _alloc_layers(self) -> None:
+        p, nl, d, f = self.prof, self.prof.n_layers, self.prof.model_dim, self.prof.ffn_dim
+        t = lambda *shape: torch.empty(shape, dtype=self.dtype, device=self.device)  # noqa: E731
+        if self.precision == "fp32":
+            self.wqkv, self.wo, self.w1, self.w2 = t(nl, d, 3 * d), t(nl, d, d), t(nl, d, f), t(nl, f, d)
+        else:
+            self.wqkv, self.wo, self.w1, self.w2 = t(nl, 3 * d, d), t(nl, d, d), t(nl, f, d), t(nl, d, f)
+
+    def _put_layer(self, l: int, x: LayerWeights) -> None:
+        self.wqkv[l].copy_(self._qkv(x))
+        self.wo[l].copy_(self._mm(x.wo))
+        self.w1[l].copy_(self._mm(x.w1))
+        self.w2[l].copy_(self._mm(x.w2))
+
+    def _put_rest(self, w) -> None:
+        """Head, conditioning and extension tensors from an object/namespace
+        with the DenoiserWeights attribute names."""
+        prof, f32 = self.prof, self._f32
+        self.w_vel = self._mm(w.w_vel)
+        self.w_audio, self.w_prompt, self.w_time = f32(w.w_audio), f32(w.w_prompt), f32(w.w_time)
+        self.w_emb = self._mm(w.w_emb) if prof.patched else None
+        self.b_emb = f32(w.b_emb) if prof.patched else None
+        if prof.adaln:
+            self.w_mod = self._mm(w.w_mod)
+            self.mod = f32(w.mod.reshape(prof.n_layers, 6 * prof.model_dim))
+            self.mod_head = f32(w.mod_head.reshape(-1))
+        else:
+            self.w_mod = self.mod = self.mod_head = None
+        self.g_q = f32(w.g_q) if prof.qk_norm else None
+        self.g_k = f32(w.g_k) if prof.qk_norm else None
+
+    @classmethod
+    def from_seed(cls, seed: int, prof: ModelProfile, precision: str, devices) -> list:
+        """The reference-seeded weights (``build_weights``, bitwise the same
+        numbers) drawn one layer at a time and uploaded to every device in
+        ``devices`` as they are drawn: host memory holds one layer, not the
+        whole model (39 GB fp32 at the 14B shape)."""
+        dws = [cls(prof, precision, torch.device(dv)) for dv in devices]
+        for dw in dws:
+            dw._alloc_layers()
+        draws = _draw_weights(seed, prof)
+        for l in range(prof.n_layers):
+            x = next(draws)
+            for dw in dws:
+                dw._put_layer(l, x)
+        rest = type("_Rest", (), {})()
+        for part in draws:
+            for k, v in part.items():
+                setattr(rest, k, v)
+        for dw in dws:
+            dw._put_rest(rest)
+        return dws
+
     @classmethod
     def from_host(cls, w: DenoiserWeights, prof: ModelProfile, precision: str, device) -> "DeviceWeights":
         dw = cls(prof, precision, torch.device(device))
-        f32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dw.device)
-
-        def mm_w(a):  # a: (in, out) fp32 host
-            if precision == "fp32":
-                return f32(a)
-            return f32(np.ascontiguousarray(np.asarray(a).T)).to(torch.bfloat16)
-
-        lw = w.layers
-        if precision == "fp32":
-            dw.wqkv = torch.stack([f32(np.concatenate([x.wq, x.wk, x.wv], axis=1)) for x in lw])
-        else:
-            dw.wqkv = torch.stack([f32(np.concatenate([x.wq.T, x.wk.T, x.wv.T], axis=0)).to(torch.bfloat16)
-                                   for x in lw])
-        dw.wo = torch.stack([mm_w(x.wo) for x in lw])
-        dw.w1 = torch.stack([mm_w(x.w1) for x in lw])
-        dw.w2 = torch.stack([mm_w(x.w2) for x in lw])
-        dw.w_vel = mm_w(w.w_vel)
-        dw.w_audio, dw.w_prompt, dw.w_time = f32(w.w_audio), f32(w.w_prompt), f32(w.w_time)
-        dw.w_emb = mm_w(w.w_emb) if prof.patched else None
-        dw.b_emb = f32(w.b_emb) if prof.patched else None
-        if prof.adaln:
-            dw.w_mod = mm_w(w.w_mod)
-            dw.mod = f32(w.mod.reshape(prof.n_layers, 6 * prof.model_dim))
-            dw.mod_head = f32(w.mod_head.reshape(-1))
-        else:
-            dw.w_mod = dw.mod = dw.mod_head = None
-        dw.g_q = f32(w.g_q) if prof.qk_norm else None
-        dw.g_k = f32(w.g_k) if prof.qk_norm else None
+        dw._alloc_layers()
+        for l, x in enumerate(w.layers):
+            dw._put_layer(l, x)
+        dw._put_rest(w)
         return dw
 
     @classmethod

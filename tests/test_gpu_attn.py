@@ -120,8 +120,8 @@ def test_segment_order_modes():
     assert rel_l2(l0.float().cpu(), a.float().cpu()) < 1e-2
 
 
-@pytest.mark.parametrize("heads", [40, 12])
-def test_full_shape_tail_split_matches_reference(heads):
+@pytest.mark.parametrize("heads,arena_order", [(40, 0), (12, 0), (40, 1), (12, 1)])
+def test_full_shape_tail_split_matches_reference(heads, arena_order):
     # 480p block: 4680 queries over [sink 1560 | 4 ring slots | current]; at
     # 40 heads the grid tail (ragged query pairs + the last units) is split
     # into KV pieces merged by the combine kernel; must agree with the
@@ -135,7 +135,9 @@ def test_full_shape_tail_split_matches_reference(heads):
     order = [3, 4, 0, 1]  # ring slots oldest -> newest, wrapped
     segs = [(0, s_tok)] + [(s_tok + n_q * s, n_q) for s in order] + [(s_tok + 2 * n_q, n_q)]
     cur = s_tok + 2 * n_q
-    desc = make_desc(7, segs, cur, n_q, 128)
+    # arena_order = 1 is the engines' benched path: the wrapped ring plus sink
+    # and current block are walked as ONE merged 24,960-row range
+    desc = make_desc(7, segs, cur, n_q, 128, arena_order=arena_order)
     scale = float(np.float32(1.0) / np.float32(np.sqrt(128)))
     n_kv = sum(n for _, n in segs)
     ws, nb = _workspace(n_q, heads)

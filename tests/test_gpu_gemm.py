@@ -277,3 +277,72 @@ def test_argument_errors_are_reported_not_launched():
     with pytest.raises(L.LivepipeError, match="channels"):
         x = torch.zeros(64, device=DEV)
         L.call("lp_codec_patch_decode", x.data_ptr(), 1, 64, 1, 1, x.data_ptr(), 1, 3, 8, x.data_ptr(), None)
+
+
+# ---- the exact benched 14B shapes: M = 4680 tokens, the
+# pair + side-stream tail split the engines use (default policy, fork on)
+
+def _qkv_14b_case(seed=11):
+    n_heads, hd, frames, gh, gw = 40, 128, 3, 30, 52
+    d, n_tok = n_heads * hd, 3 * 30 * 52
+    a, w = _ab(n_tok, d, 3 * d, seed)
+    third = hd // 6
+    t_dim, dh, dw = hd - 4 * third, 2 * third, 2 * third
+    sc, ss = spatial_tables(gh, gw, dh, dw, 10000.0)
+    return n_heads, hd, d, n_tok, a, w, t_dim, gh, gw, torch.from_numpy(sc).to(DEV), torch.from_numpy(ss).to(DEV)
+
+
+def test_qkv_epilogue_at_benched_14b_shape():
+    # 4680 x 5120 -> 15360 with 40-head RMSNorm + 3-axis RoPE + ring scatter
+    n_heads, hd, d, n_tok, a, w, t_dim, gh, gw, spc, sps = _qkv_14b_case()
+    s_tok = gh * gw
+    rows = s_tok + 5 * n_tok
+    karena = torch.zeros((rows, d), device=DEV, dtype=torch.bfloat16)
+    varena = torch.zeros_like(karena)
+    q = torch.zeros((n_tok, d), device=DEV, dtype=torch.bfloat16)
+    cur = s_tok + 3 * n_tok
+    desc = make_desc(836, [(0, s_tok), (cur, n_tok)], cur, n_tok, t_dim)
+    ddev = upload_desc(desc)
+    g_q = 1 + 0.05 * torch.randn(d, device=DEV)
+    g_k = 1 + 0.05 * torch.randn(d, device=DEV)
+    geom = L.RopeGeom(hd, t_dim // 2, s_tok, (hd - t_dim) // 2, spc.data_ptr(), sps.data_ptr())
+    epi = L.QkvEpi(d, n_heads, hd, 1, 1e-6, g_q.data_ptr(), g_k.data_ptr(), q.data_ptr(), karena.data_ptr(),
+                   varena.data_ptr(), ddev.data_ptr(), geom)
+    _gemm(a, w, None, L.EPI_QKV, L.LP_BF16, qkv=epi, fork=True)
+    y = a.float() @ w.float().T
+    qr, kr, vr = y[:, :d], y[:, d:2 * d], y[:, 2 * d:]
+
+    def norm(x, g):
+        xh = x.reshape(n_tok, n_heads, hd)
+        return (xh * torch.rsqrt((xh * xh).mean(-1, keepdim=True) + 1e-6)).reshape(n_tok, d) * g
+
+    tc = np.array(desc.rope_cos[: t_dim // 2], np.float32)
+    ts = np.array(desc.rope_sin[: t_dim // 2], np.float32)
+    qref = rope_ref(norm(qr, g_q), n_heads, hd, tc, ts, spc, sps, s_tok)
+    kref = rope_ref(norm(kr, g_k), n_heads, hd, tc, ts, spc, sps, s_tok)
+    assert rel_l2(q.float().cpu(), qref.cpu()) < 5e-3
+    assert rel_l2(karena[cur:cur + n_tok].float().cpu(), kref.cpu()) < 5e-3
+    assert rel_l2(varena[cur:cur + n_tok].float().cpu(), vr.cpu()) < 5e-3
+    # nothing outside the current block's rows is touched
+    assert karena[:cur].abs().sum().item() == 0 and karena[cur + n_tok:].abs().sum().item() == 0
+
+
+@pytest.mark.parametrize("k,n", [(5120, 5120), (13824, 5120)])
+def test_resid_at_benched_14b_shapes(k, n):
+    # O-proj (K = 5120) and FFN-down (K = 13824): gated residual into fp32 h
+    m = 4680
+    a, w = _ab(m, k, n, 12)
+    h = torch.randn((m, n), device=DEV)
+    gate = torch.randn(n, device=DEV) * 0.1
+    want = h + gate * (a.float() @ w.float().T)
+    _gemm(a, w, h, L.EPI_RESID, L.LP_F32, gate=gate, fork=True)
+    assert rel_l2(h.cpu(), want.cpu()) < 1e-5
+
+
+def test_ffn_up_gelu_at_benched_14b_shape():
+    m, k, n = 4680, 5120, 13824
+    a, w = _ab(m, k, n, 13)
+    ref = torch.nn.functional.gelu(a.float() @ w.float().T, approximate="tanh")
+    c = torch.zeros((m, n), device=DEV, dtype=torch.bfloat16)
+    _gemm(a, w, c, L.EPI_GELU, L.LP_BF16, fork=True)
+    assert rel_l2(c.float().cpu(), ref.cpu()) < 5e-3
