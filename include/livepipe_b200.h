@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LP_ABI_VERSION 2
+#define LP_ABI_VERSION 3
 
 /* status codes */
 #define LP_OK 0
@@ -145,6 +145,10 @@ typedef struct lp_euler_epi {
   float* x_out;           /* may be a peer-mapped receive slot              */
   int32_t channels, height, width, ph, pw;
   const lp_block_desc* desc;
+  const int32_t* gate_status; /* NULL, or a link status word: when it is
+                             non-zero (a failed wait on the consumer's free
+                             counter) the store is skipped, so a slot the
+                             consumer has not released is never overwritten */
 } lp_euler_epi;
 
 typedef struct lp_gemm_args {
@@ -312,10 +316,16 @@ LP_API int lp_codec_patch_encode(const float* frame, int C, int H, int W, const 
  * receive buffer (peer pointer over NVLink, or local) after waiting for the
  * slot to be free, then publishes ready.  lp_link_recv waits for ready and
  * copies out.  Waits spin on the device with a bound (timeout_ns) and poll
- * the host-mapped abort word.                                              */
+ * the host-mapped abort word.
+ * `status` (device int32, may be NULL) is STICKY: a failed wait stores
+ * LP_EABORT / LP_ETIMEOUT into it, success never clears it, and every link
+ * kernel that finds it already non-zero does nothing (no copy, no flag
+ * publish) -- so after a failure a stage neither consumes nor forwards stale
+ * data, and the host sees the first failure whenever it reads the word.  */
 LP_API int lp_link_send(const void* src, void* dst_slot, int64_t bytes, volatile uint32_t* ready_flag,
                  volatile const uint32_t* free_flag, uint32_t seq, int capacity,
-                 volatile const uint32_t* abort_word, uint64_t timeout_ns, void* stream);
+                 volatile const uint32_t* abort_word, uint64_t timeout_ns,
+                 int32_t* status, void* stream);
 LP_API int lp_link_recv(const void* src_slot, void* dst, int64_t bytes, volatile const uint32_t* ready_flag,
                  volatile uint32_t* free_flag, uint32_t seq,
                  volatile const uint32_t* abort_word, uint64_t timeout_ns,
@@ -323,10 +333,12 @@ LP_API int lp_link_recv(const void* src_slot, void* dst, int64_t bytes, volatile
 
 /* Publish `value` into a (possibly peer-mapped) flag with a system-scope
    release after all prior work on `stream` (the "ready"/"sink posted" half
-   of a link, engine.py:369 / :477-478).                                    */
-LP_API int lp_signal(volatile uint32_t* flag, uint32_t value, void* stream);
-/* Stream-ordered bounded wait until *flag >= target (engine.py:379, :439);
-   *status_out = 0, LP_EABORT or LP_ETIMEOUT (status_out may be NULL).       */
+   of a link, engine.py:369 / :477-478) -- unless gate_status is non-NULL and
+   non-zero (the stage's sticky link status: its data is not valid).        */
+LP_API int lp_signal(volatile uint32_t* flag, uint32_t value, const int32_t* gate_status, void* stream);
+/* Stream-ordered bounded wait until *flag >= target (engine.py:379, :439).
+   status_out (may be NULL) is sticky as for the links: set to LP_EABORT or
+   LP_ETIMEOUT on failure, never cleared; a non-zero word skips the wait.   */
 LP_API int lp_wait(volatile const uint32_t* flag, uint32_t target, volatile const uint32_t* abort_word,
             uint64_t timeout_ns, int32_t* status_out, void* stream);
 
@@ -337,6 +349,11 @@ LP_API int lp_wait(volatile const uint32_t* flag, uint32_t target, volatile cons
 LP_API int lp_ipc_handle(const void* dev_ptr, uint8_t* handle_out, int64_t* offset_out);
 LP_API int lp_ipc_open(const uint8_t* handle, int64_t offset, void** ptr_out);
 LP_API int lp_ipc_close(void* mapped_base);
+/* Let `device` address `peer`'s memory directly (NVLink P2P): the in-process
+   multi-device TPP runner's link kernels run on the producer's device and
+   store into the consumer's slots, and every stage polls one abort word.
+   Idempotent; LP_EUNSUPPORTED when the pair cannot peer.                    */
+LP_API int lp_peer_enable(int device, int peer);
 
 
 /* ---------------------------------------------------------------- arenas

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LIVEPIPE_LIB") or os.path.join(HERE, "liblivepipe_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "livepipe_b200.h")
 
-ABI_VERSION = 2  # LP_ABI_VERSION in include/livepipe_b200.h
+ABI_VERSION = 3  # LP_ABI_VERSION in include/livepipe_b200.h
 LP_OK, LP_EINVAL, LP_ECUDA, LP_EUNSUPPORTED, LP_ETIMEOUT, LP_EABORT = range(6)
 LP_F32, LP_BF16 = 0, 1
 EPI_STORE, EPI_RELU, EPI_GELU, EPI_RESID, EPI_QKV, EPI_EULER = range(6)
@@ -54,7 +54,7 @@ class QkvEpi(C.Structure):
 
 class EulerEpi(C.Structure):
     _fields_ = [("x_in", vp), ("x_out", vp), ("channels", i32), ("height", i32), ("width", i32), ("ph", i32),
-                ("pw", i32), ("desc", vp)]
+                ("pw", i32), ("desc", vp), ("gate_status", vp)]
 
 
 class GemmArgs(C.Structure):
@@ -100,13 +100,14 @@ _SIGS = {
     "lp_history_noise": ([vp, C.c_int, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
     "lp_randn": ([vp, i64, u64, u64, C.c_float, vp], C.c_int),
     "lp_randn_bf16": ([vp, i64, u64, u64, C.c_float, vp], C.c_int),
-    "lp_link_send": ([vp, vp, i64, vp, vp, u32, C.c_int, vp, u64, vp], C.c_int),
+    "lp_link_send": ([vp, vp, i64, vp, vp, u32, C.c_int, vp, u64, vp, vp], C.c_int),
     "lp_link_recv": ([vp, vp, i64, vp, vp, u32, vp, u64, vp, vp], C.c_int),
-    "lp_signal": ([vp, u32, vp], C.c_int),
+    "lp_signal": ([vp, u32, vp, vp], C.c_int),
     "lp_wait": ([vp, u32, vp, u64, vp, vp], C.c_int),
     "lp_ipc_handle": ([vp, vp, C.POINTER(i64)], C.c_int),
     "lp_ipc_open": ([vp, i64, C.POINTER(vp)], C.c_int),
     "lp_ipc_close": ([vp], C.c_int),
+    "lp_peer_enable": ([C.c_int, C.c_int], C.c_int),
     "lp_vmm_create": ([C.c_int, C.c_int, i64, C.POINTER(vp)], C.c_int),
     "lp_vmm_info": ([vp, C.POINTER(u64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], C.c_int),
     "lp_vmm_grow": ([vp, i64, vp], C.c_int),

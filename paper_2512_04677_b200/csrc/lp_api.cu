@@ -40,11 +40,11 @@ int unpatchify_euler(const float*, const float*, int, int, int, int, int, int, c
 int history_noise(void*, int, int, const float*, int, int, int, const lp_block_desc*, int, cudaStream_t);
 int randn(void*, int64_t, uint64_t, uint64_t, float, int, cudaStream_t);
 int link_send(const void*, void*, int64_t, volatile uint32_t*, const volatile uint32_t*, uint32_t, int,
-              const volatile uint32_t*, uint64_t, cudaStream_t);
+              const volatile uint32_t*, uint64_t, int32_t*, cudaStream_t);
 int link_recv(const void*, void*, int64_t, const volatile uint32_t*, volatile uint32_t*, uint32_t,
               const volatile uint32_t*, uint64_t, int32_t*, cudaStream_t);
 
-int signal(volatile uint32_t*, uint32_t, cudaStream_t);
+int signal(volatile uint32_t*, uint32_t, const int32_t*, cudaStream_t);
 int wait(const volatile uint32_t*, uint32_t, const volatile uint32_t*, uint64_t, int32_t*, cudaStream_t);
 int ipc_handle(const void*, uint8_t*, int64_t*);
 int ipc_open(const uint8_t*, int64_t, void**);
@@ -199,8 +199,9 @@ int lp_randn_bf16(void* out, int64_t n, uint64_t seed, uint64_t stream_id, float
 
 int lp_link_send(const void* src, void* dst_slot, int64_t bytes, volatile uint32_t* ready_flag,
                  volatile const uint32_t* free_flag, uint32_t seq, int capacity, volatile const uint32_t* abort_word,
-                 uint64_t timeout_ns, void* stream) {
-  return link_send(src, dst_slot, bytes, ready_flag, free_flag, seq, capacity, abort_word, timeout_ns, S(stream));
+                 uint64_t timeout_ns, int32_t* status, void* stream) {
+  return link_send(src, dst_slot, bytes, ready_flag, free_flag, seq, capacity, abort_word, timeout_ns, status,
+                   S(stream));
 }
 
 int lp_link_recv(const void* src_slot, void* dst, int64_t bytes, volatile const uint32_t* ready_flag,
@@ -243,11 +244,33 @@ int lp_codec_patch_encode(const float* frame, int C, int H, int W, const float* 
   return codec_patch_encode(frame, C, H, W, enc, pc, s, out, S(stream));
 }
 
-int lp_signal(volatile uint32_t* flag, uint32_t value, void* stream) { return signal(flag, value, S(stream)); }
+int lp_signal(volatile uint32_t* flag, uint32_t value, const int32_t* gate_status, void* stream) {
+  return signal(flag, value, gate_status, S(stream));
+}
 
 int lp_wait(volatile const uint32_t* flag, uint32_t target, volatile const uint32_t* abort_word, uint64_t timeout_ns,
             int32_t* status_out, void* stream) {
   return wait(flag, target, abort_word, timeout_ns, status_out, S(stream));
+}
+
+int lp_peer_enable(int device, int peer) {
+  if (device == peer) return LP_OK;
+  int can = 0;
+  LP_CUDA_TRY(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can)
+    return fail(LP_EUNSUPPORTED, "lp_peer_enable: device " + std::to_string(device) + " cannot access device " +
+                                     std::to_string(peer));
+  int prev = 0;
+  LP_CUDA_TRY(cudaGetDevice(&prev));
+  LP_CUDA_TRY(cudaSetDevice(device));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  cudaSetDevice(prev);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return LP_OK;
+  }
+  if (e != cudaSuccess) return fail(LP_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+  return LP_OK;
 }
 
 int lp_ipc_handle(const void* dev_ptr, uint8_t* handle_out, int64_t* offset_out) {

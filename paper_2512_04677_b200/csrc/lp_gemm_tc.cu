@@ -162,6 +162,8 @@ __device__ __forceinline__ void gemm_epilogue_tile(const GemmParams& p, int row,
       if (!valid) continue;
       if (p.epilogue == LP_EPI_EULER) {
         const lp_euler_epi& e = p.euler;
+        // a failed wait on the consumer's free counter: leave its slot alone
+        if (e.gate_status && *(const volatile int32_t*)e.gate_status != 0) continue;
         const float dt = e.desc->dt;
         int64_t base;
         int gy = 0, gx = 0;

@@ -44,19 +44,29 @@ __device__ int wait_geq(const volatile uint32_t* flag, uint32_t target, const vo
   return 0;
 }
 
+// Sticky status: the first failure is kept; success never clears it.
+__device__ __forceinline__ void fail_status(int32_t* status, int st) {
+  if (status && st) atomicCAS(status, 0, st);
+}
+__device__ __forceinline__ bool failed(const int32_t* status) {
+  return status && *(const volatile int32_t*)status != 0;
+}
+
 __global__ void link_send_kernel(const uint4* __restrict__ src, uint4* dst, int64_t n16, volatile uint32_t* ready,
                                  const volatile uint32_t* freef, uint32_t seq, int capacity,
-                                 const volatile uint32_t* abort_word, uint64_t timeout_ns, int* status) {
+                                 const volatile uint32_t* abort_word, uint64_t timeout_ns, int32_t* status) {
   __shared__ int st;
   if (threadIdx.x == 0) {
-    uint32_t need = seq + 1u >= (uint32_t)capacity ? seq + 1u - (uint32_t)capacity : 0u;
-    st = need ? wait_geq(freef, need, abort_word, timeout_ns) : 0;
+    if (failed(status)) {
+      st = -1;  // this stage already failed: its payload is not valid, publish nothing
+    } else {
+      uint32_t need = seq + 1u >= (uint32_t)capacity ? seq + 1u - (uint32_t)capacity : 0u;
+      st = need ? wait_geq(freef, need, abort_word, timeout_ns) : 0;
+      fail_status(status, st);
+    }
   }
   __syncthreads();
-  if (st) {
-    if (threadIdx.x == 0 && status) *status = st;
-    return;
-  }
+  if (st) return;
   for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
   __threadfence_system();
   __syncthreads();
@@ -65,32 +75,34 @@ __global__ void link_send_kernel(const uint4* __restrict__ src, uint4* dst, int6
 
 __global__ void link_recv_kernel(const uint4* src, uint4* __restrict__ dst, int64_t n16, const volatile uint32_t* ready,
                                  volatile uint32_t* freef, uint32_t seq, const volatile uint32_t* abort_word,
-                                 uint64_t timeout_ns, int* status) {
+                                 uint64_t timeout_ns, int32_t* status) {
   __shared__ int st;
-  if (threadIdx.x == 0) st = wait_geq(ready, seq + 1u, abort_word, timeout_ns);
-  __syncthreads();
-  if (st) {
-    if (threadIdx.x == 0 && status) *status = st;
-    return;
+  if (threadIdx.x == 0) {
+    if (failed(status)) {
+      st = -1;
+    } else {
+      st = wait_geq(ready, seq + 1u, abort_word, timeout_ns);
+      fail_status(status, st);
+    }
   }
+  __syncthreads();
+  if (st) return;
   for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
   __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    st_release_sys(freef, seq + 1u);
-    if (status) *status = 0;
-  }
+  if (threadIdx.x == 0) st_release_sys(freef, seq + 1u);
 }
 
-__global__ void signal_kernel(volatile uint32_t* flag, uint32_t value) {
+__global__ void signal_kernel(volatile uint32_t* flag, uint32_t value, const int32_t* gate) {
+  if (failed(gate)) return;
   __threadfence_system();
   st_release_sys(flag, value);
 }
 
 __global__ void wait_kernel(const volatile uint32_t* flag, uint32_t target, const volatile uint32_t* abort_word,
                             uint64_t timeout_ns, int32_t* status) {
-  int st = wait_geq(flag, target, abort_word, timeout_ns);
-  if (status) *status = st;
+  if (failed(status)) return;
+  fail_status(status, wait_geq(flag, target, abort_word, timeout_ns));
 }
 
 // Force-load the link kernels: with lazy module loading, the first launch of
@@ -106,11 +118,11 @@ int preload_links() {
 
 int link_send(const void* src, void* dst, int64_t bytes, volatile uint32_t* ready, const volatile uint32_t* freef,
               uint32_t seq, int capacity, const volatile uint32_t* abort_word, uint64_t timeout_ns,
-              cudaStream_t st) {
+              int32_t* status, cudaStream_t st) {
   LP_CHECK_ARG(bytes % 16 == 0, "link_send: payload must be a multiple of 16 bytes");
   LP_CHECK_ARG(capacity >= 1, "link_send: capacity >= 1");
   link_send_kernel<<<1, 1024, 0, st>>>((const uint4*)src, (uint4*)dst, bytes / 16, ready, freef, seq, capacity,
-                                       abort_word, timeout_ns, nullptr);
+                                       abort_word, timeout_ns, status);
   return launch_status("link_send");
 }
 
@@ -123,9 +135,9 @@ int link_recv(const void* src, void* dst, int64_t bytes, const volatile uint32_t
   return launch_status("link_recv");
 }
 
-int signal(volatile uint32_t* flag, uint32_t value, cudaStream_t st) {
+int signal(volatile uint32_t* flag, uint32_t value, const int32_t* gate, cudaStream_t st) {
   LP_CHECK_ARG(flag != nullptr, "lp_signal: null flag");
-  signal_kernel<<<1, 1, 0, st>>>(flag, value);
+  signal_kernel<<<1, 1, 0, st>>>(flag, value, gate);
   return launch_status("signal");
 }
 

@@ -519,14 +519,14 @@ class DeviceLink:
         self.next_send = 0
         self.next_recv = 0
 
-    def send(self, src: torch.Tensor, stream: torch.cuda.Stream, seq: int) -> None:
+    def send(self, src: torch.Tensor, stream: torch.cuda.Stream, seq: int, status: torch.Tensor) -> None:
         if seq != self.next_send:
             raise PipelineInvariantError(f"out-of-order send: expected seq {self.next_send}, got {seq}")
         self.next_send += 1
         slot = self.slots[seq % self.capacity]
         L.call("lp_link_send", src.data_ptr(), slot.data_ptr(), self.nbytes, self.flags.data_ptr(),
                self.flags.data_ptr() + 4, seq, self.capacity, self.abort.data_ptr(), self.timeout_ns,
-               stream.cuda_stream)
+               status.data_ptr(), stream.cuda_stream)
 
     def recv(self, dst: torch.Tensor, stream: torch.cuda.Stream, seq: int, status: torch.Tensor) -> None:
         if seq != self.next_recv:
@@ -568,6 +568,13 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
     nbytes = cfg.frames_per_block * prof.latent_dim * 4
     for d in sorted(set(devs)):
         prewarm_torch(f"cuda:{d}")
+    # stage k's link kernel (on its device) stores into stage k+1's slots and
+    # every stage polls the abort word on the last device: peer access
+    for a in sorted(set(devs)):
+        for b in sorted(set(devs)):
+            if a != b:
+                L.init_device(a)
+                L.call("lp_peer_enable", a, b)
     abort = torch.zeros(4, dtype=torch.int32, device=f"cuda:{last_dev}")
     streams = [torch.cuda.Stream(d) for d in devs]
     stages = [Stage(cfg, rt, T - k + 1, devs[k - 1], streams[k - 1]) for k in range(1, T + 1)]
@@ -601,7 +608,10 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
     # every device buffer the workers touch exists before the first thread
     # starts: an allocation while another stage's link kernel spins may wait
     # on the device
+    # one sticky link status word per stage (recv and send of that stage), and
+    # a pinned host mirror the worker polls once per block without a sync
     statuses = [torch.zeros(1, dtype=torch.int32, device=f"cuda:{st.device}") for st in stages]
+    mirrors = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in stages]
     dec_buf = torch.zeros((cfg.frames_per_block, prof.latent_dim), dtype=torch.float32, device=f"cuda:{last_dev}")
     dec_status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{last_dev}")
     dec_stream = torch.cuda.Stream(last_dev)
@@ -616,9 +626,12 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
     def stage_worker(k: int) -> None:
         st = stages[k - 1]
         sink = SinkSlot(rt.conditions.reference.copy(), cfg.sink_delta)
-        status = statuses[k - 1]
+        status, mirror = statuses[k - 1], mirrors[k - 1]
         try:
             for i in range(cfg.blocks):
+                if int(mirror[0]) != 0:
+                    raise PipelineInvariantError(f"stage {k} link wait failed with status {int(mirror[0])} "
+                                                 f"(seen before block {i})")
                 if i == 1:
                     while True:
                         if abort_evt.is_set():
@@ -638,7 +651,8 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
                         links[k - 2].recv(st.fw.x_in, st.stream, i, status)
                     st.prepare(i)
                     st.forward(i)
-                    links[k - 1].send(st.fw.x_out, st.stream, i)
+                    links[k - 1].send(st.fw.x_out, st.stream, i, status)
+                    mirror.copy_(status, non_blocking=True)
         except BaseException as exc:  # noqa: BLE001 - worker boundary
             fail(exc)
 
@@ -677,6 +691,9 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
         torch.cuda.synchronize(d)
     if errors:
         raise errors[0]
+    bad = [(k + 1, int(s.item())) for k, s in enumerate(statuses) if int(s.item()) != 0]
+    if bad:
+        raise PipelineInvariantError(f"stage link waits failed (stage, status): {bad}")
     nfe = sum(st.nfe for st in stages)
     dev0 = devs[0]
     tl = ()

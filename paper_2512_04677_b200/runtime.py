@@ -550,7 +550,7 @@ class Forward:
             # velocity head with the flow step fused into the GEMM epilogue (K6)
             ph, pw = prof.patch if prof.patched else (0, 0)
             self._euler = L.EulerEpi(self.x_in.data_ptr(), xo_ptr, prof.channels, prof.height, prof.width,
-                                     ph, pw, self.desc_ptr)
+                                     ph, pw, self.desc_ptr, self.euler_gate)
             args = L.GemmArgs()
             args.in_dtype, args.out_dtype, args.epilogue = self.dw.ldt, L.LP_F32, L.EPI_EULER
             args.m, args.n, args.k = N, prof.out_dim, d
@@ -560,6 +560,9 @@ class Forward:
             L.call("lp_gemm", C.byref(args), st)
 
     _sigma_on = False
+    # device address of a sticky link status word (TPP fused send): the
+    # Euler epilogue skips its store into the peer slot when it is non-zero
+    euler_gate = None
 
     def _tag(self, tag: str, phase: str, stream) -> None:
         if self.probe:

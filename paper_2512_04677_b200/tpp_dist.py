@@ -208,12 +208,12 @@ class IpcLink:
             raise PipelineInvariantError(f"FIFO violated: expected sequence {self.next_seq}, got {seq}")
         self.next_seq += 1
 
-    def send(self, src: torch.Tensor, stream: torch.cuda.Stream, seq: int) -> None:
+    def send(self, src: torch.Tensor, stream: torch.cuda.Stream, seq: int, status: torch.Tensor) -> None:
         self._check(seq)
         slots, flags = self.peer[0], self.peer[1]
         dst = slots + (seq % self.capacity) * self.nbytes
         L.call("lp_link_send", src.data_ptr(), dst, self.nbytes, flags, flags + 4, seq, self.capacity,
-               self.abort_ptr, self.timeout_ns, stream.cuda_stream)
+               self.abort_ptr, self.timeout_ns, status.data_ptr(), stream.cuda_stream)
 
     def recv(self, dst: torch.Tensor, stream: torch.cuda.Stream, seq: int, status: torch.Tensor) -> None:
         self._check(seq)
@@ -276,6 +276,7 @@ class DecodeBackend:
         self.shape = (cfg.frames_per_block, prof.latent_dim)
         self.buf = torch.zeros(self.shape, dtype=torch.float32, device=f"cuda:{device}")
         self.status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{device}")
+        self.status_host = torch.zeros(1, dtype=torch.int32).pin_memory()
         self.stages = []
         self.fused = None
 
@@ -290,6 +291,9 @@ class DecodeBackend:
 
     def recv(self, link: "IpcLink", i: int) -> None:
         link.recv(self.buf, self.stream, i, self.status)
+
+    def mirror_status(self) -> None:
+        _mirror(self.status, self.status_host, self.stream, self.device)
 
     def read_output(self, out: torch.Tensor | None = None) -> np.ndarray | None:
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
@@ -320,7 +324,11 @@ class DeviceBackend:
         self.stages = [Stage(cfg, rt, j, device, self.stream) for j in role.steps]
         prof = cfg.model_profile
         self.shape = (cfg.frames_per_block, prof.latent_dim)
+        # sticky link status (lp_link_*): written by failed device waits,
+        # gates every later send / fused store / ready publish of this rank;
+        # mirrored to pinned host memory once per block for a cheap host poll
         self.status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{device}")
+        self.status_host = torch.zeros(1, dtype=torch.int32).pin_memory()
         # double-buffered send staging: block i's x' leaves from sendbuf[i % 2]
         self.sendbuf = torch.zeros((2,) + self.shape, dtype=torch.float32, device=f"cuda:{device}")
         self.sent = [None, None]
@@ -359,6 +367,7 @@ class DeviceBackend:
         per slot); a device wait on the slot's ``free`` counter precedes the
         forward and a system-scope release of ``ready`` follows it."""
         slots = [link.peer[0] + s * link.nbytes for s in range(link.capacity)]
+        self.stages[-1].fw.euler_gate = self.status.data_ptr()  # baked into the captured epilogue args
         self.stages[-1].ensure_out_graphs(slots)
         self.fused = (link, slots)
 
@@ -378,7 +387,7 @@ class DeviceBackend:
                         L.call("lp_wait", flags + 4, need, link.abort_ptr, link.timeout_ns, self.status.data_ptr(),
                                self.stream.cuda_stream)
                     st.forward(i, timed=timed, out_ptr=slots[i % link.capacity])
-                    L.call("lp_signal", flags, i + 1, self.stream.cuda_stream)
+                    L.call("lp_signal", flags, i + 1, self.status.data_ptr(), self.stream.cuda_stream)
                 else:
                     st.forward(i, timed=timed)
                 prev = st
@@ -395,13 +404,16 @@ class DeviceBackend:
                 ready = torch.cuda.Event()
                 ready.record(self.stream)
             self.side.wait_event(ready)
-            link.send(self.sendbuf[b], self.side, i)
+            link.send(self.sendbuf[b], self.side, i, self.status)
             done = torch.cuda.Event()
             done.record(self.side)
             self.sent[b] = done
 
     def recv(self, link: IpcLink, i: int) -> None:
         link.recv(self.x_in, self.stream, i, self.status)
+
+    def mirror_status(self) -> None:
+        _mirror(self.status, self.status_host, self.stream, self.device)
 
     def read_output(self, out: torch.Tensor | None = None) -> np.ndarray | None:
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
@@ -517,7 +529,7 @@ class DistTPP:
         s = torch.cuda.Stream(self.device)
         for p in self.peer_aborts + [self.abort.data_ptr()]:
             try:
-                L.call("lp_signal", p, 1, s.cuda_stream)
+                L.call("lp_signal", p, 1, None, s.cuda_stream)
             except L.LivepipeError:
                 pass
 
@@ -563,6 +575,7 @@ class DistTPP:
         the final LatentBlock on the last rank when it is read to the host."""
         if i != self.blocks_in:
             raise PipelineInvariantError(f"blocks must be submitted in order: expected {self.blocks_in}, got {i}")
+        self._poll_status(i)
         self.blocks_in += 1
         self._maybe_receive_sink(i)
         if self.role.first:
@@ -579,6 +592,8 @@ class DistTPP:
         if not self.role.last:
             if not (self.fused_send and self.backend.fused is not None):
                 self._send(i)
+            if self.transport == "ipc":
+                self.backend.mirror_status()
             return None
         if out is not None and i != 0:
             self.backend.read_output(out)
@@ -590,6 +605,17 @@ class DistTPP:
         if i == 0:
             self._aas_last(xb)
         return xb
+
+    def _poll_status(self, i: int) -> None:
+        """Per-block host check of the sticky link status, as of the last
+        mirror copy that has landed (no device synchronisation): a failed
+        wait on this rank surfaces at the next block instead of at finish()."""
+        if self.transport != "ipc":
+            return
+        st = int(self.backend.status_host[0])
+        if st != 0:
+            raise PipelineInvariantError(f"rank {self.rank}: stage link wait failed with status {st} "
+                                         f"(seen before block {i})")
 
     # -- whole rollout -------------------------------------------------------
     def run(self) -> RolloutResult | None:
@@ -640,6 +666,12 @@ class DistTPP:
         for h in getattr(self, "_abort_handles", []):
             _ipc_release(h)
         self._abort_handles = []
+
+
+def _mirror(status: torch.Tensor, host: torch.Tensor, stream: torch.cuda.Stream, device: int) -> None:
+    """Enqueue a copy of the device status word into its pinned host mirror."""
+    with torch.cuda.device(device), torch.cuda.stream(stream):
+        host.copy_(status, non_blocking=True)
 
 
 def _with_devices(cfg: EngineConfig, devices: tuple) -> EngineConfig:

@@ -122,9 +122,37 @@ def main():
         fused = bool(kw.pop("fused", 1))
         if kw.pop("profile", None) == "wan_small":
             kw["profile"] = wan_small()
+        stall = (int(kw.pop("stall_rank", -1)), int(kw.pop("stall_block", -1)), float(kw.pop("stall_s", 0.0)))
         cfg = lp.EngineConfig(mode="tpp", precision=prec, devices=(dev,), **kw)
-        res = tpp_dist.run_tpp_dist(cfg, transport="ipc", device=dev, fused_send=fused, decode_gpu=decode_gpu)
         role = tpp_dist.pipeline_layout(world, cfg.steps, decode_gpu)[rank]
+        if stall[0] < 0:
+            res = tpp_dist.run_tpp_dist(cfg, transport="ipc", device=dev, fused_send=fused, decode_gpu=decode_gpu)
+        else:
+            # injected failure: rank stall[0] stops consuming for stall[2] s
+            # before block stall[1] (longer than link_timeout_s); every rank
+            # records what it raised and the blocks it completed
+            import time
+
+            res = None
+            runner = tpp_dist.DistTPP(cfg, transport="ipc", device=dev, fused_send=fused)
+            done, err = [], None
+            try:
+                for i in range(cfg.blocks):
+                    if rank == stall[0] and i == stall[1]:
+                        time.sleep(stall[2])
+                    xb = runner.step(i)
+                    if xb is not None:
+                        done.append(np.asarray(xb.values, np.float32))
+                runner.finish()
+            except lp.PipelineInvariantError as e:
+                err = str(e)
+                runner.abort_peers()
+            torch.cuda.synchronize(dev)
+            with open(f"{out}.rank{rank}", "w") as f:
+                json.dump({"rank": rank, "error": err, "blocks_done": len(done)}, f)
+            if done:
+                np.save(f"{out}.rank{rank}.npy", np.stack(done))
+            runner.close()
     if res is not None:
         lat = np.stack([np.asarray(b.values, np.float32) for b in res.blocks])
         rec = {"latents_sha256": hashlib.sha256(O.latents_bytes(list(lat))).hexdigest(), "nfe": res.nfe,

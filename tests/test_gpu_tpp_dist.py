@@ -97,3 +97,25 @@ def test_ipc_two_pipelines_of_four_ranks(tmp_path):
         cfg = dataclasses.replace(cfg, noise_seed=tpp_dist.pipe_noise_seed(cfg, pipe))
         seq = lp.run_sequential(cfg)
         assert got.tobytes() == np.stack([b.values for b in seq.blocks]).tobytes(), pipe
+
+
+def test_ipc_tpp_stalled_consumer_raises_and_keeps_unconsumed_slot(tmp_path):
+    # injected failure (engine.py:425-429 abort propagation): rank 1 (the
+    # consumer) stops consuming for 6 s before block 2 with a 2 s link
+    # timeout.  Rank 0's fused send for block 3 times out on the slot's free
+    # counter: the sticky status gates its Euler-epilogue store and ready
+    # publish, so block 2's latent -- sent but not yet consumed -- is NOT
+    # overwritten; rank 1 then receives block 2 intact and fails on block 3.
+    # Both ranks raise PipelineInvariantError.
+    kw = dict(steps=4, blocks=6, cache_capacity=2)
+    out = tmp_path / "res"
+    launch(2, "gpu", out, dict(kw, precision="bf16", profile="wan_small", link_timeout_s=2.0, fused=1,
+                               stall_rank=1, stall_block=2, stall_s=6.0), timeout=600)
+    r0 = json.load(open(f"{out}.rank0"))
+    r1 = json.load(open(f"{out}.rank1"))
+    assert r0["error"] and "status" in r0["error"], r0
+    assert r1["error"], r1
+    assert r1["blocks_done"] == 3, r1  # blocks 0, 1 and the unconsumed block 2
+    got = np.load(f"{out}.rank1.npy")
+    seq = lp.run_sequential(lp.EngineConfig(mode="sequential", precision="bf16", profile=wan_small(), **kw))
+    assert got.tobytes() == np.stack([b.values for b in seq.blocks[:3]]).tobytes()
