@@ -49,6 +49,13 @@ def parse():
                     help="N>1: one dedicated decode rank per pipeline (the paper's 4 DiT + 1 VAE layout)")
     ap.add_argument("--history-sigma", type=float, default=0.0,
                     help="history-noise sigma (config 4: corrupted cache views, device Philox noise)")
+    ap.add_argument("--api", default="stream", choices=["stream", "dropin"],
+                    help="dropin: the reference-facing B200Denoiser.denoise_block loop (host latents per call, "
+                         "the reference engine's run_sequential driving order) instead of the streaming engine")
+    ap.add_argument("--long-horizon", type=int, default=0, metavar="BLOCKS",
+                    help="config 4: one stream of BLOCKS blocks (834 = 10k video frames) from a cold start: "
+                         "whole-run and steady FPS, measured TTFF, per-block latency, drift, ring replay")
+    ap.add_argument("--history-mode", default="fixed", choices=["fixed", "scaled"])
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N>1 (gloo lets several ranks share one GPU in tests)")
     return ap.parse_args()
@@ -519,10 +526,182 @@ def run_dist(args, rank, world, local):
     dist.destroy_process_group()
 
 
+def run_dropin(args):
+    """FPS through the drop-in plug point the reference engine calls
+    (Runtime.denoiser.denoise_block, engine.py:269-277), driven in the
+    reference's run_sequential order (engine.py:255-285): per block and step
+    a host latent in, a host velocity out, flow_step on the host, the
+    KvEntry pushed into the reference-semantics RollingKvCache.  Every call
+    synchronises (the plug-in contract returns numpy), so this is an
+    end-to-end number by construction; timed by the host clock."""
+    import numpy as np
+    import torch
+
+    import paper_2512_04677_b200 as lp
+    from paper_2512_04677_b200.model import DeviceWeights
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    prof = profile_for(args.config)
+    T, Lc = 4, 4
+    sched = lp.TimestepSchedule.uniform(T)
+    dw = DeviceWeights.random(prof, "bf16", f"cuda:{dev}", 7)
+    dn = lp.B200Denoiser(None, sched, precision="bf16", device_weights=dw)
+    K, W = args.steps, max(args.warmup, Lc + 1)
+    conds = lp.synthetic_conditions(11, W + K, prof.audio_dim, prof.prompt_dim, prof.latent_dim)
+    caches = {j: lp.RollingKvCache(j, Lc) for j in range(1, T + 1)}
+    sink = lp.SinkSlot(conds.reference.copy(), 1)
+    rng = np.random.default_rng(11)
+    h2d = d2h = 0
+
+    def block(i):
+        nonlocal h2d, d2h
+        x = lp.LatentBlock(rng.standard_normal((3, prof.latent_dim), dtype=np.float32), i)
+        for j in range(T, 0, -1):
+            o = dn.denoise_block(x, j, caches[j].view(), lp.BlockCond(conds.audio_for(i), conds.prompt),
+                                 sink.content, i + 1, max_entries=Lc)
+            h2d += x.values.nbytes
+            d2h += o.velocity.nbytes
+            x = lp.flow_step(x, o.velocity, sched.dt)
+            caches[j].push(o.kv)
+        return x
+
+    for i in range(W):  # warm-up: fills the windows (steady N_kv from block L on)
+        block(i)
+    torch.cuda.synchronize(dev)
+    h2d = d2h = 0
+    with ClockSampler(dev) as clk:
+        t0 = time.perf_counter()
+        for i in range(W, W + K):
+            block(i)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t0
+    fps = FRAMES_PER_BLOCK_VIDEO * K / wall
+    line = {"metric": "streaming FPS through the drop-in denoise_block (reference engine loop order), 1 GPU",
+            "value": fps, "unit": "FPS", "n_gpus": 1, "steps": K, "warmup": W, "ms_per_step": 1e3 * wall / K,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic latents/audio, random-init weights", "api": "dropin",
+            "config": {"workload": workload(args.config), "path": "B200Denoiser.denoise_block x T per block, "
+                       "host numpy latents, host flow_step, RollingKvCache window L=4 (N_kv 24,960 steady)"},
+            "e2e": {"value": fps, "unit": "FPS", "h2d_bytes_per_step": h2d // K, "d2h_bytes_per_step": d2h // K,
+                    "timer": "host perf_counter (every call synchronises)"},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
+def run_long(args):
+    """BASELINE config 4: a 14B-shape stream of ``--long-horizon`` blocks
+    with RSFM (sink at i + delta, RoPE positions growing to N + 1, fp64
+    angles), the rolling window and history noise, from a cold start:
+
+    * TTFF = submit of block 0 -> its 12 frames decoded on the device,
+      including the first (eager) forwards, the one-shot AAS sink swap and
+      the graph capture that follows it (engine.py:255-285, PAPER.md TTFF);
+    * whole-run FPS = 12 N / (stream start -> last block decoded);
+      steady FPS over blocks > L (full window);
+    * per-block latency from CUDA events on the pipeline stream;
+    * drift = cosine similarity of every decoded frame with the decoded sink
+      frame (metrics.drift_metric, engine.py:238), first vs last 10 %;
+    * every block finite; the ring slots replayed against the reference
+      window rule (RollingKvCache, kvcache.py:41-56) at every block."""
+    import numpy as np
+    import torch
+
+    import paper_2512_04677_b200 as lp
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    prof = profile_for(args.config)
+    T, Lc, N = 4, 4, args.long_horizon
+    sigma = args.history_sigma
+    cfg = lp.EngineConfig(mode="sequential", steps=T, cache_capacity=Lc, frames_per_block=3, profile=prof,
+                          precision="bf16", devices=(dev,), device_inputs=True, blocks=N, history_sigma=sigma,
+                          history_mode=args.history_mode)
+    pipe = lp.StreamingPipeline(cfg)
+    s = pipe.stream
+    codec = lp.PatchVideoCodec(7, prof.channels, prof.height, prof.width, 3, 8, 4)
+    dc = lp.DeviceCodec(codec, dev)
+    lat = prof.latent_dim
+    g = torch.Generator(device=f"cuda:{dev}").manual_seed(11)
+    noise = torch.empty((3, lat), device=f"cuda:{dev}")
+    frames = torch.empty((12, codec.pixel_dim), device=f"cuda:{dev}")
+    drift = torch.empty((N, 12), device=f"cuda:{dev}")
+    finite = torch.ones((), dtype=torch.bool, device=f"cuda:{dev}")
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(N)]
+    window = []  # reference replay: append, pop(0) beyond capacity
+
+    def sink_frame():
+        sk = torch.from_numpy(np.asarray(pipe.sink.content, np.float32)).to(f"cuda:{dev}").reshape(1, lat)
+        out = torch.empty((4, codec.pixel_dim), device=f"cuda:{dev}")
+        dc.decode_into(sk, out, s)
+        return out[0]
+
+    def one(i, ref):
+        with torch.cuda.stream(s):
+            noise.normal_(generator=g)
+        ev[i][0].record(s)
+        x = pipe.submit(i, noise)
+        with torch.cuda.stream(s):
+            dc.decode_into(x.reshape(3, lat), frames, s)
+            drift[i] = (frames @ ref) / (frames.norm(dim=1) * ref.norm())
+            finite.logical_and_(torch.isfinite(x).all())
+        ev[i][1].record(s)
+        window.append(i)
+        if len(window) > Lc:
+            window.pop(0)
+        for st in pipe.stages.values():
+            if st.ring.blocks != window:
+                raise AssertionError(f"ring replay diverged at block {i}: {st.ring.blocks} vs {window}")
+        return x
+
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_start.record(s)
+        x0 = one(0, sink_frame())
+        pipe.aas(x0)  # host round trip: part of the first-block bubble
+        ref = sink_frame()  # drift reference: the swapped sink
+        pipe.capture()
+        t_first = torch.cuda.Event(enable_timing=True)
+        t_first.record(s)
+        for i in range(1, N):
+            one(i, ref)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_end.record(s)
+        torch.cuda.synchronize(dev)
+    total_s = t_start.elapsed_time(t_end) / 1e3
+    ttff_ms = t_start.elapsed_time(t_first)
+    lat_ms = np.array([a.elapsed_time(b) for a, b in ev])
+    steady = lat_ms[Lc + 1:] if N > Lc + 2 else lat_ms[1:]
+    d = drift.float().cpu().numpy()
+    k = max(1, N // 10)
+    line = {"metric": "long-horizon stream (BASELINE config 4): whole-run FPS", "value": 12 * N / total_s,
+            "unit": "FPS", "n_gpus": 1, "steps": N, "warmup": 0, "ms_per_step": 1e3 * total_s / N,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic noise (device Philox), random-init weights", "api": "stream",
+            "config": {"workload": workload(args.config) + f", {N} blocks = {12 * N} video frames from a cold start",
+                       "history_sigma": sigma, "history_mode": args.history_mode, "window": Lc,
+                       "sink_positions": [1 + 1, N + 1]},
+            "fps_steady": 12e3 / float(np.mean(steady)), "ttff_ms": ttff_ms,
+            "ttff_note": "block 0 (eager) + decode + AAS sink swap + graph capture",
+            "block_ms": {"p50": float(np.percentile(steady, 50)), "p99": float(np.percentile(steady, 99)),
+                         "max": float(steady.max())},
+            "drift": {"first_10pct_mean": float(d[:k].mean()), "last_10pct_mean": float(d[-k:].mean()),
+                      "min": float(d.min()), "finite": bool(np.isfinite(d).all())},
+            "all_blocks_finite": bool(finite.item()), "ring_replay": "ok",
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    if args.long_horizon:
+        run_long(args)
+        return
     if args.impl == "reference":
         run_reference(args)
+    elif args.api == "dropin":
+        run_dropin(args)
     else:
         run_ours(args)
 

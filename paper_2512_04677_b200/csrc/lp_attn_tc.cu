@@ -49,6 +49,9 @@ using namespace sm100;
 #ifndef LP_ATTN_POLY
 #define LP_ATTN_POLY 3  // pairs of every 8 whose exp2 runs as the FMA-pipe polynomial (sweep: r1c, r1j)
 #endif
+#ifndef LP_ATTN_POLY_WIN
+#define LP_ATTN_POLY_WIN 3  // ... in the bounded-exponent kernel (cheaper polynomial: no clamps)
+#endif
 
 constexpr int AT_M = 128;      // query rows per softmax warpgroup
 constexpr int AT_N = 128;      // keys per tile
@@ -83,6 +86,8 @@ struct AttnParams {
   int split;      // KV pieces per split unit
   float* part_o;  // [piece][256][128] unnormalised O of split units
   float* part_ml; // [piece][256][2]   (running max in log2 units, row sum)
+  int* flags;     // [grid] bounded-exponent kernel: 1 = a row left the exponent
+                  // window, rerun exactly; exact kernel: non-null = rerun only those
 };
 
 // Unit u -> (head, pair): regular units (both Q tiles valid) first, head-major
@@ -137,6 +142,42 @@ __device__ __forceinline__ uint64_t ex2_poly2(uint64_t xv) {
   const uint64_t magic = f32x2(12582912.0f, 12582912.0f);
   const uint64_t t = fadd2_rm(xv, magic);
   const uint64_t f = fsub2(xv, fsub2(t, magic));
+  uint64_t q = ffma2(f32x2(0.07706641f, 0.07706641f), f, f32x2(0.2276457f, 0.2276457f));
+  q = ffma2(q, f, f32x2(0.69511662f, 0.69511662f));
+  q = ffma2(q, f, f32x2(1.0f, 1.0f));
+  float q0, q1, t0, t1;
+  unpack_f32x2(q, q0, q1);
+  unpack_f32x2(t, t0, t1);
+  return f32x2(__int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23)),
+               __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23)));
+}
+
+// fma.f32x2 has no .sat form: two scalar FFMA.SAT (still no FMNMX clamps)
+__device__ __forceinline__ uint64_t ffma2_sat(uint64_t a, uint64_t b, uint64_t c) {
+  float a0, a1, b0, b1, c0, c1;
+  unpack_f32x2(a, a0, a1);
+  unpack_f32x2(b, b0, b1);
+  unpack_f32x2(c, c0, c1);
+  return f32x2(__saturatef(fmaf(a0, b0, c0)), __saturatef(fmaf(a1, b1, c1)));
+}
+__device__ __forceinline__ uint64_t ffma2_rm(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+// 2^x for a pair of raw scores s with x = s*scale*log2e - m clamped to
+// [-127, 65] for free: the first FMA computes y = (x + 127) / 192 with .sat
+// (y in [0, 1]), so no FMNMX clamps are needed.  floor(x) comes from a
+// round-down FMA into the 1.5*2^23 magic range, the fraction from one more
+// FMA, 2^f from the degree-3 polynomial and the exponent is added as an
+// integer.  At x = -127 the result is exactly +0 (masked keys); at the upper
+// clamp 2^65 is returned and the caller's window check (row sum < 2^64) fails.
+__device__ __forceinline__ uint64_t ex2_poly2_win(uint64_t s2, uint64_t a2, uint64_t b2) {
+  const uint64_t y = ffma2_sat(s2, a2, b2);
+  const uint64_t k192 = f32x2(192.0f, 192.0f), cm = f32x2(12582912.0f - 127.0f, 12582912.0f - 127.0f);
+  const uint64_t t = ffma2_rm(y, k192, cm);
+  const uint64_t f = ffma2(y, k192, fsub2(cm, t));
   uint64_t q = ffma2(f32x2(0.07706641f, 0.07706641f), f, f32x2(0.2276457f, 0.2276457f));
   q = ffma2(q, f, f32x2(0.69511662f, 0.69511662f));
   q = ffma2(q, f, f32x2(1.0f, 1.0f));
@@ -211,9 +252,19 @@ __device__ __forceinline__ void tmem_st32_x(uint32_t taddr, const uint32_t* r) {
       "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
 }
 
+// FAST = the bounded-exponent form: each row's exponent offset m is the exact
+// max of its FIRST KV tile and is never updated, so the per-tile row max, the
+// O rescale and the exponent clamps leave the softmax critical path.  This is
+// exact softmax (the offset cancels in O / l) whenever every later score stays
+// within 2^64 of 2^m; a row that leaves that window shows up as a row sum
+// >= 2^64 (or inf), flags its CTA, and the exact kernel (!FAST, running only
+// the flagged CTAs) recomputes that work unit with the online max.  Wan's
+// q/k RMSNorm bounds |s| by |q||k|/sqrt(d), far inside the window.
+template <bool FAST>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  if (!FAST && p.flags != nullptr && p.flags[blockIdx.x] == 0) return;  // rerun only flagged units
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AttnSmem::BAR_OFF);
@@ -230,6 +281,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   int* seg_row = reinterpret_cast<int*>(smem + AttnSmem::SEG_OFF);
   int* seg_len = seg_row + LP_MAX_SEG;
   int* n_seg_s = seg_len + LP_MAX_SEG;
+  int* win_flag = n_seg_s + 3;  // FAST: some row left the exponent window
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   int unit, piece = -1;
@@ -287,6 +339,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const int t1 = piece < 0 ? nt : (int)((int64_t)nt * (piece + 1) / p.split);
     n_seg_s[1] = t1 - t0;
     n_seg_s[2] = t0;
+    *win_flag = 0;
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -465,6 +518,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         for (int i = 0; i < 128; ++i)
           if (i >= nvalid) s[i] = __float_as_uint(-INFINITY);
       }
+      float alpha = 1.0f;
+      bool rescale = false;
+      if (!FAST || j == 0) {
       // row max as a tree: 8 independent 3-input max chains, then 8 -> 1
       float mq[8];
 #pragma unroll
@@ -476,8 +532,6 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       const float mx = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
                              fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
       const float m_tile = mx * sc;
-      float alpha = 1.0f;
-      bool rescale = false;
       if (j == 0) {
         m_run = m_tile;
       } else {
@@ -488,10 +542,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           m_run = m_tile;
         }
       }
+      }
       // p = 2^(s*scale*log2e - m), packed to bf16 pairs in key order.
       // Pairs go through the packed fp32x2 FMA pipe (FFMA2/FADD2); 3 of
       // every 8 pairs take the polynomial exp2, the rest MUFU.EX2.
       const uint64_t sc2 = f32x2(sc, sc), nm2 = f32x2(-m_run, -m_run);
+      const float wa = sc * (1.0f / 192.0f), wb = (127.0f - m_run) * (1.0f / 192.0f);
+      const uint64_t wa2 = f32x2(wa, wa), wb2 = f32x2(wb, wb);
       uint64_t rs2[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) rs2[k] = f32x2(0.f, 0.f);
@@ -499,12 +556,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       auto exp_pairs = [&](int i0) {
 #pragma unroll
         for (int i = i0; i < i0 + 64; i += 2) {
-          const bool poly = ((i >> 1) & 7) >= 8 - LP_ATTN_POLY;
-          const uint64_t a = ffma2(f32x2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sc2, nm2);
+          const bool poly = ((i >> 1) & 7) >= 8 - (FAST ? LP_ATTN_POLY_WIN : LP_ATTN_POLY);
+          const uint64_t sv2 = f32x2(__uint_as_float(s[i]), __uint_as_float(s[i + 1]));
           uint64_t e;
-          if (poly) {
-            e = ex2_poly2(a);
+          if (FAST && poly) {
+            e = ex2_poly2_win(sv2, wa2, wb2);
+          } else if (poly) {
+            e = ex2_poly2(ffma2(sv2, sc2, nm2));
           } else {
+            const uint64_t a = ffma2(sv2, sc2, nm2);
             float a0, a1;
             unpack_f32x2(a, a0, a1);
             e = f32x2(ex2(a0), ex2(a1));
@@ -518,7 +578,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       // keys [0, 64): P columns [0, 32); O is rescaled before P(j).V starts
       exp_pairs(0);
       tmem_st32_x(t_s + 0, &s[0]);
-      if (rescale) {
+      if (!FAST && rescale) {
         // P(j-1).V is complete (implied by s_full(j)); O_x is idle until p_half(j)
 #pragma unroll 1
         for (int c0 = 0; c0 < AT_D; c0 += 32) {
@@ -539,13 +599,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       float r[8];
 #pragma unroll
       for (int k = 0; k < 4; ++k) unpack_f32x2(rs2[k], r[2 * k], r[2 * k + 1]);
-      l_run = l_run * alpha + (((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7])));
+      const float rsum = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+      l_run = FAST ? l_run + rsum : l_run * alpha + rsum;
       tmem_st32_x(t_s + 32, &s[32]);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[x]);
     }
+    if (FAST && active && __any_sync(0xffffffffu, !(l_run < 0x1p64f)) && lane == 0) atomicOr(win_flag, 1);
     // epilogue: O / l -> bf16 (whole unit) or unnormalised (O, m, l) partials
     if (active) {
     mbar_wait(o_done, 0);
@@ -598,6 +660,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
   }
+  if (FAST && threadIdx.x == 0) p.flags[blockIdx.x] = *win_flag;
 }
 
 // Merge the KV-range partials of the split units in piece order:
@@ -636,7 +699,8 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnParams p) {
 
 int preload_attn_tc() {
   cudaFuncAttributes a;
-  LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_tc_kernel));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_tc_kernel<true>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_tc_kernel<false>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_combine_kernel));
   return LP_OK;
 }
@@ -708,10 +772,14 @@ static AttnPlan plan_attention(int n_q, int n_heads, int sms) {
   return bp;
 }
 
+// Workspace: [KV-split partials O | (m, l)] then one window flag per CTA.
+static int64_t partial_bytes(const AttnPlan& pl) { return pl.pieces() * (2 * AT_M) * (AT_D + 2) * 4; }
+static int64_t flag_bytes(int grid) { return ((int64_t)grid * 4 + 255) / 256 * 256; }
+
 int64_t attention_workspace_bytes(int n_q, int n_heads) {
   if (n_q <= 0 || n_heads <= 0 || num_sms() <= 0) return 0;
   const AttnPlan pl = plan_attention(n_q, n_heads, num_sms());
-  return pl.pieces() * (2 * AT_M) * (AT_D + 2) * 4;
+  return partial_bytes(pl) + flag_bytes(pl.grid());
 }
 
 int attention_tc(const lp_attn_args* a, cudaStream_t st) {
@@ -727,11 +795,13 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
   rc = make_tmap_bf16_2d(&tv, a->v_arena, (uint64_t)a->arena_rows, (uint64_t)d, (uint64_t)d, AT_N, 64);
   if (rc) return rc;
   AttnPlan pl = plan_attention(a->n_q, a->n_heads, num_sms());
-  const int64_t need = pl.pieces() * (2 * AT_M) * (AT_D + 2) * 4;
-  if (pl.pieces() > 0 && (a->workspace == nullptr || a->workspace_bytes < need)) {
-    pl.n_whole = pl.n_units;  // no workspace: run every unit whole
+  const int64_t have = a->workspace ? a->workspace_bytes : 0;
+  if (pl.pieces() > 0 && have < partial_bytes(pl) + flag_bytes(pl.grid())) {
+    pl.n_whole = pl.n_units;  // no (or too small a) workspace: run every unit whole
     pl.split = 1;
   }
+  // the bounded-exponent kernel needs the flag words (after the partials)
+  const bool fast = have >= partial_bytes(pl) + flag_bytes(pl.grid()) && getenv("LP_ATTN_EXACT") == nullptr;
   AttnParams p;
   p.n_q = a->n_q;
   p.n_heads = a->n_heads;
@@ -745,9 +815,18 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
   p.split = pl.split;
   p.part_o = static_cast<float*>(a->workspace);
   p.part_ml = p.part_o ? p.part_o + pl.pieces() * (2 * AT_M) * AT_D : nullptr;
+  p.flags = fast ? reinterpret_cast<int*>(static_cast<char*>(a->workspace) + partial_bytes(pl)) : nullptr;
   const int smem = AttnSmem::TOTAL;
-  LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  attn_tc_kernel<<<pl.grid(), AT_THREADS, smem, st>>>(tq, tk, tv, p);
+  if (fast) {
+    LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attn_tc_kernel<true><<<pl.grid(), AT_THREADS, smem, st>>>(tq, tk, tv, p);
+    rc = launch_status("attention_tc_window");
+    if (rc) return rc;
+  }
+  // exact online-max kernel: every unit, or (after the bounded-exponent
+  // kernel) only the units it flagged -- the others exit on their first load
+  LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  attn_tc_kernel<false><<<pl.grid(), AT_THREADS, smem, st>>>(tq, tk, tv, p);
   rc = launch_status("attention_tc");
   if (rc || pl.n_whole == pl.n_units) return rc;
   const int64_t warps = (int64_t)(pl.n_units - pl.n_whole) * (2 * AT_M);

@@ -44,9 +44,15 @@ __device__ int wait_geq(const volatile uint32_t* flag, uint32_t target, const vo
   return 0;
 }
 
-// Sticky status: the first failure is kept; success never clears it.
+// Sticky status: the first failure is kept; success never clears it.  The
+// word may live in pinned host memory (the threaded engine polls it there
+// with no device->host copy in the stage streams), so no atomics: every
+// writer of one word runs on one stream, and any non-zero code is a failure.
 __device__ __forceinline__ void fail_status(int32_t* status, int st) {
-  if (status && st) atomicCAS(status, 0, st);
+  if (status && st && *(volatile int32_t*)status == 0) {
+    *(volatile int32_t*)status = st;
+    __threadfence_system();
+  }
 }
 __device__ __forceinline__ bool failed(const int32_t* status) {
   return status && *(const volatile int32_t*)status != 0;

@@ -238,12 +238,17 @@ class B200Denoiser:
 
     def __init__(self, weights: DenoiserWeights, schedule: TimestepSchedule, rope_base: float = 10000.0, *,
                  precision: str = "fp32", device=None, profile: ModelProfile | None = None,
-                 max_live_entries: int | None = None):
+                 max_live_entries: int | None = None, device_weights: DeviceWeights | None = None):
         if precision not in ("fp32", "bf16"):
             raise ValueError("precision must be 'fp32' or 'bf16'")
         self.weights = weights
         self.schedule = schedule
         self.rope_base = rope_base
+        if device_weights is not None:  # weights already resident (e.g. drawn on the device)
+            if device_weights.precision != precision:
+                raise ValueError(f"device_weights are {device_weights.precision}, precision is {precision}")
+            profile = profile or device_weights.prof
+            device = device if device is not None else device_weights.device
         prof = profile or getattr(weights, "profile", None)
         if prof is None or (not prof.patched and prof.model_dim != weights.model_dim):
             prof = toy_profile(len(weights.layers), weights.n_heads, weights.head_dim,
@@ -257,7 +262,8 @@ class B200Denoiser:
         self.precision = precision
         self.device = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
         L.init_device(self.device.index or 0)
-        self.dw = DeviceWeights.from_host(weights, prof, precision, self.device)
+        self.dw = (device_weights if device_weights is not None
+                   else DeviceWeights.from_host(weights, prof, precision, self.device))
         self._lock = threading.Lock()
         self._pool = None
         self._ws = {}

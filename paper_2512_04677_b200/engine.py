@@ -608,12 +608,15 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
     # every device buffer the workers touch exists before the first thread
     # starts: an allocation while another stage's link kernel spins may wait
     # on the device
-    # one sticky link status word per stage (recv and send of that stage), and
-    # a pinned host mirror the worker polls once per block without a sync
-    statuses = [torch.zeros(1, dtype=torch.int32, device=f"cuda:{st.device}") for st in stages]
-    mirrors = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in stages]
+    # one sticky link status word per stage (recv and send of that stage) in
+    # pinned, device-mapped host memory: the link kernels write a failure
+    # straight into it and the worker polls it once per block.  No
+    # device->host copy is enqueued on the stage streams -- such copies share
+    # the copy engine's queue across streams, and a copy queued behind a
+    # spinning link kernel can block the very stage that kernel waits for.
+    statuses = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in stages]
     dec_buf = torch.zeros((cfg.frames_per_block, prof.latent_dim), dtype=torch.float32, device=f"cuda:{last_dev}")
-    dec_status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{last_dev}")
+    dec_status = torch.zeros(1, dtype=torch.int32).pin_memory()
     dec_stream = torch.cuda.Stream(last_dev)
     for st in stages:  # the reference sink (its projection scratch is allocated here, not mid-stream)
         st.set_sink(rt.conditions.reference.copy())
@@ -626,11 +629,11 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
     def stage_worker(k: int) -> None:
         st = stages[k - 1]
         sink = SinkSlot(rt.conditions.reference.copy(), cfg.sink_delta)
-        status, mirror = statuses[k - 1], mirrors[k - 1]
+        status = statuses[k - 1]
         try:
             for i in range(cfg.blocks):
-                if int(mirror[0]) != 0:
-                    raise PipelineInvariantError(f"stage {k} link wait failed with status {int(mirror[0])} "
+                if int(status[0]) != 0:
+                    raise PipelineInvariantError(f"stage {k} link wait failed with status {int(status[0])} "
                                                  f"(seen before block {i})")
                 if i == 1:
                     while True:
@@ -652,7 +655,6 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
                     st.prepare(i)
                     st.forward(i)
                     links[k - 1].send(st.fw.x_out, st.stream, i, status)
-                    mirror.copy_(status, non_blocking=True)
         except BaseException as exc:  # noqa: BLE001 - worker boundary
             fail(exc)
 
@@ -667,8 +669,8 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
                     ev.record(stream)
                 wait_event(ev)
                 host = buf.cpu()
-                if int(status.cpu().item()) != 0:
-                    raise PipelineInvariantError(f"decoder link wait failed with status {int(status.item())}")
+                if int(status[0]) != 0:
+                    raise PipelineInvariantError(f"decoder link wait failed with status {int(status[0])}")
                 ds = time.perf_counter() - t0_host
                 xb = LatentBlock(host.numpy(), i)
                 out_blocks[i] = xb
@@ -691,7 +693,7 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
         torch.cuda.synchronize(d)
     if errors:
         raise errors[0]
-    bad = [(k + 1, int(s.item())) for k, s in enumerate(statuses) if int(s.item()) != 0]
+    bad = [(k + 1, int(s[0])) for k, s in enumerate(statuses) if int(s[0]) != 0]
     if bad:
         raise PipelineInvariantError(f"stage link waits failed (stage, status): {bad}")
     nfe = sum(st.nfe for st in stages)

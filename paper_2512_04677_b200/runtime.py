@@ -608,7 +608,9 @@ class Forward:
             n += 2
         if prof.adaln:
             n += 4
-        per_layer = 7 + (1 if self.fp32 else 0) + (2 if self._sigma_on else 0) + (1 if self.attn_ws_bytes else 0)
+        # with a workspace the attention is the bounded-exponent kernel + the
+        # exact rerun of flagged units (+ the combine of the KV-split tail)
+        per_layer = 7 + (1 if self.fp32 else 0) + (2 if self._sigma_on else 0) + (2 if self.attn_ws_bytes else 0)
         return n + prof.n_layers * per_layer + (3 if (self.fp32 or not self.fuse_euler) else 2)
 
     def velocity_host(self) -> np.ndarray:

@@ -275,8 +275,7 @@ class DecodeBackend:
         self.stream = torch.cuda.Stream(device)
         self.shape = (cfg.frames_per_block, prof.latent_dim)
         self.buf = torch.zeros(self.shape, dtype=torch.float32, device=f"cuda:{device}")
-        self.status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{device}")
-        self.status_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self.status = _status_word()
         self.stages = []
         self.fused = None
 
@@ -291,9 +290,6 @@ class DecodeBackend:
 
     def recv(self, link: "IpcLink", i: int) -> None:
         link.recv(self.buf, self.stream, i, self.status)
-
-    def mirror_status(self) -> None:
-        _mirror(self.status, self.status_host, self.stream, self.device)
 
     def read_output(self, out: torch.Tensor | None = None) -> np.ndarray | None:
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
@@ -326,9 +322,8 @@ class DeviceBackend:
         self.shape = (cfg.frames_per_block, prof.latent_dim)
         # sticky link status (lp_link_*): written by failed device waits,
         # gates every later send / fused store / ready publish of this rank;
-        # mirrored to pinned host memory once per block for a cheap host poll
-        self.status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{device}")
-        self.status_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        # lives in pinned host memory, so the host polls it with no copy
+        self.status = _status_word()
         # double-buffered send staging: block i's x' leaves from sendbuf[i % 2]
         self.sendbuf = torch.zeros((2,) + self.shape, dtype=torch.float32, device=f"cuda:{device}")
         self.sent = [None, None]
@@ -411,9 +406,6 @@ class DeviceBackend:
 
     def recv(self, link: IpcLink, i: int) -> None:
         link.recv(self.x_in, self.stream, i, self.status)
-
-    def mirror_status(self) -> None:
-        _mirror(self.status, self.status_host, self.stream, self.device)
 
     def read_output(self, out: torch.Tensor | None = None) -> np.ndarray | None:
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
@@ -592,8 +584,6 @@ class DistTPP:
         if not self.role.last:
             if not (self.fused_send and self.backend.fused is not None):
                 self._send(i)
-            if self.transport == "ipc":
-                self.backend.mirror_status()
             return None
         if out is not None and i != 0:
             self.backend.read_output(out)
@@ -608,11 +598,11 @@ class DistTPP:
 
     def _poll_status(self, i: int) -> None:
         """Per-block host check of the sticky link status, as of the last
-        mirror copy that has landed (no device synchronisation): a failed
+        device write that has landed (no device synchronisation): a failed
         wait on this rank surfaces at the next block instead of at finish()."""
         if self.transport != "ipc":
             return
-        st = int(self.backend.status_host[0])
+        st = int(self.backend.status[0])
         if st != 0:
             raise PipelineInvariantError(f"rank {self.rank}: stage link wait failed with status {st} "
                                          f"(seen before block {i})")
@@ -668,10 +658,14 @@ class DistTPP:
         self._abort_handles = []
 
 
-def _mirror(status: torch.Tensor, host: torch.Tensor, stream: torch.cuda.Stream, device: int) -> None:
-    """Enqueue a copy of the device status word into its pinned host mirror."""
-    with torch.cuda.device(device), torch.cuda.stream(stream):
-        host.copy_(status, non_blocking=True)
+def _status_word() -> torch.Tensor:
+    """A sticky link status word in pinned host memory.  Pinned memory is
+    device-mapped at the same address (UVA), so the link kernels write a
+    failure code straight into it and the host polls it without enqueueing a
+    device->host copy: such a copy shares the copy engine's queue with other
+    streams and, queued behind a spinning link kernel, can stall the stage
+    that kernel is waiting for."""
+    return torch.zeros(1, dtype=torch.int32).pin_memory()
 
 
 def _with_devices(cfg: EngineConfig, devices: tuple) -> EngineConfig:

@@ -152,6 +152,40 @@ def test_full_shape_tail_split_matches_reference(heads, arena_order):
     assert torch.equal(tc, tc2)
 
 
+def test_exponent_window_fallback(monkeypatch):
+    # The bounded-exponent kernel fixes each row's exponent offset at the max
+    # of its first KV tile.  Head 0 gets a block of "hot" keys in a later
+    # tile whose scores sit ~98 log2 units above it (outside the 2^64
+    # window): those work units must be flagged and recomputed by the exact
+    # online-max kernel, while head 1 (ordinary scores) stays on the bounded
+    # kernel.  Both match fp32 torch.
+    heads, n_q, d, rows = 2, 300, 256, 2000
+    g = torch.Generator(device=DEV).manual_seed(21)
+    ka = torch.randn((rows, d), generator=g, device=DEV)
+    va = torch.randn((rows, d), generator=g, device=DEV).to(torch.bfloat16)
+    q = torch.randn((n_q, d), generator=g, device=DEV) * 0.5
+    q[:, :128] += 1.0
+    ka[1500:1510, :128] = 6.0  # s ~ 128*6/sqrt(128) = 68 nats above the sink tile's max
+    ka, q = ka.to(torch.bfloat16), q.to(torch.bfloat16)
+    segs = [(0, 130), (1400, 300), (1700, n_q)]
+    scale = float(np.float32(1.0) / np.float32(np.sqrt(128)))
+    desc = make_desc(5, segs, 1700, n_q, 128, arena_order=1)
+    n_kv = sum(n for _, n in segs)
+    ref = _ref(q, ka, va, segs, heads, scale)
+    fast = _run("lp_attention", q, ka, va, desc, heads, scale, n_kv)
+    monkeypatch.setenv("LP_ATTN_EXACT", "1")
+    exact = _run("lp_attention", q, ka, va, desc, heads, scale, n_kv)
+    monkeypatch.delenv("LP_ATTN_EXACT")
+    for h in range(heads):
+        sl = slice(h * 128, (h + 1) * 128)
+        assert rel_l2(fast[:, sl].float().cpu(), ref[:, sl].cpu()) < 1e-2, h
+        assert rel_l2(exact[:, sl].float().cpu(), ref[:, sl].cpu()) < 1e-2, h
+    # without the rerun, head 0's hot keys would be weighted by the clamped
+    # exponentials (2^65 on the polynomial pairs vs 2^94 on MUFU ones) and
+    # miss the reference by O(1); head 1 ran the bounded kernel itself
+    assert not torch.equal(fast[:, 128:], exact[:, 128:])
+
+
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 def test_device_history_noise_moments(dtype):
     # kvcache.py:121-137 with the device Philox stream (perf runs): the

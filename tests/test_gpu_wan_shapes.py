@@ -81,11 +81,15 @@ def test_14b_depth_rollout_matches_oracle():
     assert len(errs) == 6 and max(errs) < TOL_BF16, errs
 
 
+@pytest.mark.timeout(1200)
 def test_1p3b_full_config_bf16_matches_fp32_validation_path():
+    # 5 blocks: block 4 is the first to attend over the full window
+    # (sink + 4 ring slots + current, N_kv = 24,960); the fp32 validation
+    # kernels are SIMT pinned-order, minutes at this shape
     prof = lp.WAN_1_3B
-    kw = dict(mode="sequential", profile=prof, steps=4, blocks=6, cache_capacity=4)
+    kw = dict(mode="sequential", profile=prof, steps=4, blocks=5, cache_capacity=4)
     bf = _run(lp.EngineConfig(precision="bf16", **kw))
     fp = _run(lp.EngineConfig(precision="fp32", **kw))
     errs = [rel_l2(a, b) for a, b in zip(bf, fp)]
     _log("wan_1p3b_full", "bf16_vs_fp32", errs)
-    assert len(errs) == 6 and max(errs) < TOL_BF16, errs
+    assert len(errs) == 5 and max(errs) < TOL_BF16, errs
