@@ -86,8 +86,9 @@ struct AttnParams {
   int split;      // KV pieces per split unit
   float* part_o;  // [piece][256][128] unnormalised O of split units
   float* part_ml; // [piece][256][2]   (running max in log2 units, row sum)
-  int* flags;     // [grid] bounded-exponent kernel: 1 = a row left the exponent
-                  // window, rerun exactly; exact kernel: non-null = rerun only those
+  int* flags;     // bounded-exponent kernels: 1 = a row left the exponent window,
+                  // rerun exactly; exact kernel: non-null = rerun only those
+  int flag_pairs; // flags written per CTA of a cluster pair (2 per work unit)
 };
 
 // Unit u -> (head, pair): regular units (both Q tiles valid) first, head-major
@@ -252,6 +253,52 @@ __device__ __forceinline__ void tmem_st32_x(uint32_t taddr, const uint32_t* r) {
       "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
 }
 
+// Thread 0: the descriptor's segments (merged in arena-row order when the
+// descriptor says so) and this CTA's KV tile range -> shared memory.
+__device__ void plan_segments(const AttnParams& p, int piece, int* seg_row, int* seg_len, int* n_seg_s) {
+  // Key order does not change softmax(QK^T)V, so with desc->arena_order
+  // the segments are visited in arena-row order with physically adjacent
+  // ones merged: in steady state [sink | L+1 ring slots] is one contiguous
+  // range and only its last tile is ragged (24,960 keys: 195 tiles instead
+  // of 198 segment-by-segment).  Deterministic for a given row placement
+  // (the engines' ring slots depend only on the block index: TPP == seq);
+  // without it, logical order, so the drop-in's pool placement is invisible.
+  const int n_in = min(p.desc->n_seg, LP_MAX_SEG);
+  const bool by_row = p.desc->arena_order != 0;
+  int nseg = 0;
+  for (int s = 0; s < n_in; ++s) {
+    const int r = p.desc->seg_row[s], l = p.desc->seg_len[s];
+    if (l <= 0) continue;
+    int i = nseg++;
+    while (by_row && i > 0 && seg_row[i - 1] > r) {
+      seg_row[i] = seg_row[i - 1];
+      seg_len[i] = seg_len[i - 1];
+      --i;
+    }
+    seg_row[i] = r;
+    seg_len[i] = l;
+  }
+  int merged = 0;
+  for (int s = 0; s < nseg; ++s) {
+    if (by_row && merged > 0 && seg_row[merged - 1] + seg_len[merged - 1] == seg_row[s]) {
+      seg_len[merged - 1] += seg_len[s];
+    } else {
+      seg_row[merged] = seg_row[s];
+      seg_len[merged] = seg_len[s];
+      ++merged;
+    }
+  }
+  nseg = merged;
+  int nt = 0;
+  for (int s = 0; s < nseg; ++s) nt += (seg_len[s] + AT_N - 1) / AT_N;
+  n_seg_s[0] = nseg;
+  // this CTA's KV tile range: all tiles, or piece `piece` of `split`
+  const int t0 = piece < 0 ? 0 : (int)((int64_t)nt * piece / p.split);
+  const int t1 = piece < 0 ? nt : (int)((int64_t)nt * (piece + 1) / p.split);
+  n_seg_s[1] = t1 - t0;
+  n_seg_s[2] = t0;
+}
+
 // FAST = the bounded-exponent form: each row's exponent offset m is the exact
 // max of its FIRST KV tile and is never updated, so the per-tile row max, the
 // O rescale and the exponent clamps leave the softmax critical path.  This is
@@ -264,7 +311,9 @@ template <bool FAST>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
-  if (!FAST && p.flags != nullptr && p.flags[blockIdx.x] == 0) return;  // rerun only flagged units
+  if (!FAST && p.flags != nullptr &&
+      (p.flag_pairs ? (p.flags[2 * blockIdx.x] | p.flags[2 * blockIdx.x + 1]) : p.flags[blockIdx.x]) == 0)
+    return;  // rerun only flagged units
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AttnSmem::BAR_OFF);
@@ -298,47 +347,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   const bool two = q0 + AT_M < p.n_q;  // tile B holds valid rows
 
   if (threadIdx.x == 0) {
-    // Key order does not change softmax(QK^T)V, so with desc->arena_order
-    // the segments are visited in arena-row order with physically adjacent
-    // ones merged: in steady state [sink | L+1 ring slots] is one contiguous
-    // range and only its last tile is ragged (24,960 keys: 195 tiles instead
-    // of 198 segment-by-segment).  Deterministic for a given row placement
-    // (the engines' ring slots depend only on the block index: TPP == seq);
-    // without it, logical order, so the drop-in's pool placement is invisible.
-    const int n_in = min(p.desc->n_seg, LP_MAX_SEG);
-    const bool by_row = p.desc->arena_order != 0;
-    int nseg = 0;
-    for (int s = 0; s < n_in; ++s) {
-      const int r = p.desc->seg_row[s], l = p.desc->seg_len[s];
-      if (l <= 0) continue;
-      int i = nseg++;
-      while (by_row && i > 0 && seg_row[i - 1] > r) {
-        seg_row[i] = seg_row[i - 1];
-        seg_len[i] = seg_len[i - 1];
-        --i;
-      }
-      seg_row[i] = r;
-      seg_len[i] = l;
-    }
-    int merged = 0;
-    for (int s = 0; s < nseg; ++s) {
-      if (by_row && merged > 0 && seg_row[merged - 1] + seg_len[merged - 1] == seg_row[s]) {
-        seg_len[merged - 1] += seg_len[s];
-      } else {
-        seg_row[merged] = seg_row[s];
-        seg_len[merged] = seg_len[s];
-        ++merged;
-      }
-    }
-    nseg = merged;
-    int nt = 0;
-    for (int s = 0; s < nseg; ++s) nt += (seg_len[s] + AT_N - 1) / AT_N;
-    n_seg_s[0] = nseg;
-    // this CTA's KV tile range: all tiles, or piece `piece` of `split`
-    const int t0 = piece < 0 ? 0 : (int)((int64_t)nt * piece / p.split);
-    const int t1 = piece < 0 ? nt : (int)((int64_t)nt * (piece + 1) / p.split);
-    n_seg_s[1] = t1 - t0;
-    n_seg_s[2] = t0;
+    plan_segments(p, piece, seg_row, seg_len, n_seg_s);
     *win_flag = 0;
   }
   if (warp == 0 && lane == 0) {
@@ -663,6 +672,348 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   if (FAST && threadIdx.x == 0) p.flags[blockIdx.x] = *win_flag;
 }
 
+// ---------------------------------------------------------------------------
+// Cluster-pair attention (tcgen05.mma.cta_group::2), the product kernel.
+//
+// A work unit (256 queries of one head[, one KV range]) runs on a CTA pair:
+// each CTA owns 128 query rows (its TMEM lanes) and loads HALF of every K/V
+// tile -- K: 64 of the 128 keys, all 128 dims; V: all 128 keys, 64 of the
+// dims -- so each SM streams half the K/V bytes of the single-CTA kernel, and
+// the leader issues M = 256 MMAs for the pair.  With one Q tile per SM the
+// TMEM holds two S buffers, O and two P buffers:
+//   S0 [0,128)  S1 [128,256)  O [256,384)  P0 [384,448)  P1 [448,512)
+// so S(j+2) is issued as soon as the softmax has LOADED S(j) (s_free), before
+// its exponentials: the tensor core runs S(j+2) while softmax(j) computes and
+// PV(j) once P(j) is stored.  Nothing on the tensor pipe waits on the softmax
+// latency, only on its throughput.  Two softmax warpgroups per CTA split the
+// 128 keys of a tile (64 each, all 128 rows by TMEM lane quarter): with the
+// bounded-exponent offset (max of the first tile, exchanged once) they never
+// synchronise per tile; their row sums are added at the end.
+//   warp 0      TMA producer (both CTAs): Q once, K/V halves (4-stage rings),
+//               completion counted on the leader's barriers
+//   warp 1      TMEM allocation (both), MMA issue (leader only)
+//   warps 4-7   softmax keys [0, 64)    warps 8-11  softmax keys [64, 128)
+constexpr int A2_KS = 4, A2_VS = 4;          // K / V ring stages
+constexpr int A2_KT = 64 * AT_D * 2;         // 16 KB: this CTA's 64 keys x 128 dims
+constexpr int A2_KHALF = 64 * 64 * 2;        // 8 KB: one 64-dim SW128 block of it
+constexpr int A2_VT = AT_N * 64 * 2;         // 16 KB: 128 keys x this CTA's 64 dims
+
+struct Attn2Smem {
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = Q_OFF + AT_TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + A2_KS * A2_KT;
+  static constexpr int BAR_OFF = V_OFF + A2_VS * A2_VT;
+  static constexpr int XCH_OFF = BAR_OFF + 512;
+  static constexpr int SEG_OFF = XCH_OFF + 2 * AT_M * 4;
+  static constexpr int TOTAL = SEG_OFF + 2 * LP_MAX_SEG * 4 + 16 + 1024;
+};
+
+__device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
+    attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Attn2Smem::BAR_OFF);
+  uint64_t* q_full = bars;               // leader's copy used
+  uint64_t* k_full = bars + 1;           // [KS] leader
+  uint64_t* k_empty = k_full + A2_KS;    // [KS] both (multicast commit)
+  uint64_t* v_full = k_empty + A2_KS;    // [VS] leader
+  uint64_t* v_empty = v_full + A2_VS;    // [VS] both
+  uint64_t* s_full = v_empty + A2_VS;    // [2] both
+  uint64_t* s_free = s_full + 2;         // [2] leader: 8 softmax warps x 2 CTAs loaded S
+  uint64_t* p_lo = s_free + 2;           // [2] leader: keys [0,64) of P stored (4 warps x 2 CTAs)
+  uint64_t* p_hi = p_lo + 2;             // [2] leader: keys [64,128)
+  uint64_t* pv_done = p_hi + 2;          // [2] both: P buffer consumed
+  uint64_t* o_done = pv_done + 2;        // both
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+  float* xch = reinterpret_cast<float*>(smem + Attn2Smem::XCH_OFF);  // [2][128] per-row exchange
+  int* seg_row = reinterpret_cast<int*>(smem + Attn2Smem::SEG_OFF);
+  int* seg_len = seg_row + LP_MAX_SEG;
+  int* n_seg_s = seg_len + LP_MAX_SEG;
+  int* win_flag = n_seg_s + 3;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const int c = blockIdx.x >> 1;
+  int unit, piece = -1;
+  if (c < p.n_whole) {
+    unit = c;
+  } else {
+    const int v = c - p.n_whole;
+    unit = p.n_whole + v / p.split;
+    piece = v % p.split;
+  }
+  int head, pair;
+  unit_coords(p, unit, head, pair);
+  const int q0 = pair * (2 * AT_M) + (int)rank * AT_M;  // this CTA's first query row
+
+  if (threadIdx.x == 0) {
+    plan_segments(p, piece, seg_row, seg_len, n_seg_s);
+    *win_flag = 0;
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < A2_KS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < A2_VS; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 16);
+      mbar_init(&p_lo[i], 8);
+      mbar_init(&p_hi[i], 8);
+      mbar_init(&pv_done[i], 1);
+    }
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+  }
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / TMA
+  if (warp == 1) tmem_alloc_2cta(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int n_tiles = n_seg_s[1];
+  const int t_first = n_seg_s[2];
+  const int col0 = head * AT_D;
+
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(AT_REG_CTRL));
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer (both CTAs)
+    if (elect_one()) {
+      const uint64_t pol = l2_policy_evict_last();
+      uint8_t* sq = smem + Attn2Smem::Q_OFF;
+      if (rank == 0) mbar_arrive_expect_tx(q_full, 2 * AT_TILE_BYTES);
+      tma_load_2d_2sm(sq, &tmQ, q_full, col0, q0, pol);
+      tma_load_2d_2sm(sq + AT_HALF, &tmQ, q_full, col0 + 64, q0, pol);
+      TileCursor cur;
+      cur.init(seg_row, seg_len, n_seg_s[0]);
+      cur.skip(t_first);
+      for (int t = 0; t < n_tiles; ++t, cur.next()) {
+        const int ks = t % A2_KS, vs = t % A2_VS;
+        mbar_wait(&k_empty[ks], ((t / A2_KS) & 1) ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(&k_full[ks], 2 * A2_KT);
+        uint8_t* sk = smem + Attn2Smem::K_OFF + ks * A2_KT;
+        const int krow = cur.cur_row() + 64 * (int)rank;  // this CTA's 64 keys of the tile
+        tma_load_2d_2sm(sk, &tmK, &k_full[ks], col0, krow, pol);
+        tma_load_2d_2sm(sk + A2_KHALF, &tmK, &k_full[ks], col0 + 64, krow, pol);
+        mbar_wait(&v_empty[vs], ((t / A2_VS) & 1) ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(&v_full[vs], 2 * A2_VT);
+        tma_load_2d_2sm(smem + Attn2Smem::V_OFF + vs * A2_VT, &tmV, &v_full[vs], col0 + 64 * (int)rank,
+                        cur.cur_row(), pol);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (leader)
+    if (rank == 0) {
+      constexpr uint32_t IDESC_S = idesc_bf16_f32(2 * AT_M, AT_N);               // Q K^T, both K-major
+      constexpr uint32_t IDESC_O = idesc_bf16_f32(2 * AT_M, AT_D, false, true);  // P V: P in TMEM, V MN-major
+      const uint32_t sq = smem_u32(smem + Attn2Smem::Q_OFF);
+      auto issue_s = [&](int t) {  // S_{t&1} = Q K_t^T
+        const uint32_t sk = smem_u32(smem + Attn2Smem::K_OFF + (t % A2_KS) * A2_KT);
+#pragma unroll
+        for (int kk = 0; kk < AT_D / 16; ++kk)
+          mma_bf16_ss_2cta(tmem_base + (t & 1) * AT_N,
+                           sdesc_kmajor_sw128(sq + (kk >> 2) * AT_HALF + (kk & 3) * 32),
+                           sdesc_kmajor_sw128(sk + (kk >> 2) * A2_KHALF + (kk & 3) * 32), IDESC_S, kk != 0);
+        mma_commit_2cta_mc(&s_full[t & 1]);
+        mma_commit_2cta_mc(&k_empty[t % A2_KS]);
+      };
+      auto issue_pv = [&](int t, int h) {  // O += P_{t&1}[keys 64h..] V_t[64h..]
+        const uint32_t sv = smem_u32(smem + Attn2Smem::V_OFF + (t % A2_VS) * A2_VT);
+        const uint32_t tp = tmem_base + 384 + (t & 1) * 64;
+#pragma unroll
+        for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
+          mma_bf16_ts_2cta(tmem_base + 256, tp + kk * 8, sdesc_mnmajor_sw128(sv + kk * 16 * 128, A2_VT), IDESC_O,
+                           (t | kk) != 0);
+      };
+      mbar_wait(q_full, 0);
+      for (int t = 0; t < min(2, n_tiles); ++t) {
+        mbar_wait(&k_full[t % A2_KS], (t / A2_KS) & 1);
+        tc_fence_after();
+        if (elect_one()) issue_s(t);
+        __syncwarp();
+      }
+      for (int j = 0; j < n_tiles; ++j) {
+        const int b = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        if (j + 2 < n_tiles) {  // S(j+2) into S_b as soon as softmax(j) has loaded S(j)
+          mbar_wait(&s_free[b], ph);
+          mbar_wait(&k_full[(j + 2) % A2_KS], ((j + 2) / A2_KS) & 1);
+          tc_fence_after();
+          if (elect_one()) issue_s(j + 2);
+          __syncwarp();
+        }
+        mbar_wait(&v_full[j % A2_VS], (j / A2_VS) & 1);
+        mbar_wait(&p_lo[b], ph);
+        tc_fence_after();
+        if (elect_one()) issue_pv(j, 0);
+        __syncwarp();
+        mbar_wait(&p_hi[b], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          issue_pv(j, 1);
+          mma_commit_2cta_mc(&pv_done[b]);
+          mma_commit_2cta_mc(&v_empty[j % A2_VS]);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) mma_commit_2cta_mc(o_done);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ softmax (both CTAs)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(AT_REG_SOFTMAX));
+    const int w = (warp - 4) / 4;        // key half of every tile
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;   // row within this CTA's 128 == TMEM lane
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t t_s = tmem_base + lane_base + 64 * w;
+    const uint32_t t_p = tmem_base + lane_base + 384 + 32 * w;
+    const uint32_t t_o = tmem_base + lane_base + 256;
+    const float sc = p.scale_log2;
+    float m_run = 0.0f, l_run = 0.0f;
+    uint64_t wa2 = 0, wb2 = 0, sc2 = f32x2(sc, sc), nm2 = 0;
+    TileCursor cs;
+    cs.init(seg_row, seg_len, n_seg_s[0]);
+    cs.skip(t_first);
+    for (int j = 0; j < n_tiles; ++j, cs.next()) {
+      const int b = j & 1;
+      const uint32_t ph = (j >> 1) & 1;
+      const int nvalid = cs.cur_valid() - 64 * w;  // valid keys of this warp's half
+      mbar_wait(&s_full[b], ph);
+      tc_fence_after();
+      uint32_t s[64];
+      tmem_ld32(t_s + b * AT_N, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+      tmem_ld32(t_s + b * AT_N + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&s_free[b], 0);
+      if (nvalid < 64) {  // ragged segment tail (warp-uniform)
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (i >= nvalid) s[i] = __float_as_uint(-INFINITY);
+      }
+      if (j == 0) {  // the row's exponent offset: max of the first tile, both key halves
+        float mq[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mq[k] = __uint_as_float(s[k]);
+#pragma unroll
+        for (int i = 8; i < 64; i += 8)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mq[k] = fmaxf(mq[k], __uint_as_float(s[i + k]));
+        xch[w * AT_M + r] = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
+                                  fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
+        softmax_bar();
+        m_run = fmaxf(xch[r], xch[AT_M + r]) * sc;
+        const float wa = sc * (1.0f / 192.0f), wb = (127.0f - m_run) * (1.0f / 192.0f);
+        wa2 = f32x2(wa, wa);
+        wb2 = f32x2(wb, wb);
+        nm2 = f32x2(-m_run, -m_run);
+      }
+      if (j >= 2) mbar_wait(&pv_done[b], ph ^ 1);  // P_b of tile j-2 consumed
+      uint64_t rs2[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) rs2[k] = f32x2(0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 64; i += 2) {
+        const bool poly = ((i >> 1) & 7) >= 8 - LP_ATTN_POLY_WIN;
+        const uint64_t sv2 = f32x2(__uint_as_float(s[i]), __uint_as_float(s[i + 1]));
+        uint64_t e;
+        if (poly) {
+          e = ex2_poly2_win(sv2, wa2, wb2);
+        } else {
+          const uint64_t a = ffma2(sv2, sc2, nm2);
+          float a0, a1;
+          unpack_f32x2(a, a0, a1);
+          e = f32x2(ex2(a0), ex2(a1));
+        }
+        rs2[(i >> 1) & 3] = fadd2(rs2[(i >> 1) & 3], e);
+        float e0, e1;
+        unpack_f32x2(e, e0, e1);
+        s[i / 2] = pack_bf16(e0, e1);
+      }
+      tmem_st32_x(t_p + b * 64, &s[0]);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(w == 0 ? &p_lo[b] : &p_hi[b], 0);
+      float rr[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) unpack_f32x2(rs2[k], rr[2 * k], rr[2 * k + 1]);
+      l_run += ((rr[0] + rr[1]) + (rr[2] + rr[3])) + ((rr[4] + rr[5]) + (rr[6] + rr[7]));
+    }
+    // epilogue: the row sum of both key halves, then O / l (or partials);
+    // each warpgroup stores 64 of the 128 output columns of its rows
+    mbar_wait(o_done, 0);
+    tc_fence_after();
+    softmax_bar();  // every read of xch (first-tile max) is done
+    xch[w * AT_M + r] = l_run;
+    softmax_bar();
+    const float l_tot = xch[r] + xch[AT_M + r];
+    const int row = q0 + r;
+    const bool valid = row < p.n_q;
+    if (w == 0 && __any_sync(0xffffffffu, valid && !(l_tot < 0x1p64f)) && lane == 0) atomicOr(win_flag, 1);
+    if (piece >= 0) {
+      const int64_t slot = (int64_t)(c - p.n_whole) * (2 * AT_M) + (int)rank * AT_M + r;
+      float* po = p.part_o + slot * AT_D;
+#pragma unroll 1
+      for (int c0 = 64 * w; c0 < 64 * w + 64; c0 += 32) {
+        uint32_t v[32];
+        if (n_tiles > 0) {
+          tmem_ld32(t_o + c0, v);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0u;
+        }
+        float4* o = reinterpret_cast<float4*>(po + c0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          o[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                             __uint_as_float(v[4 * q + 3]));
+      }
+      if (w == 0) reinterpret_cast<float2*>(p.part_ml)[slot] = make_float2(n_tiles > 0 ? m_run : -INFINITY, l_tot);
+    } else {
+      const float inv_l = l_tot > 0.0f ? 1.0f / l_tot : 0.0f;
+#pragma unroll 1
+      for (int c0 = 64 * w; c0 < 64 * w + 64; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(t_o + c0, v);
+        tmem_ld_wait();
+        if (valid) {
+          uint4* o = reinterpret_cast<uint4*>(p.out + (int64_t)row * p.ldo + col0 + c0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            o[q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q]) * inv_l, __uint_as_float(v[8 * q + 1]) * inv_l),
+                              pack_bf16(__uint_as_float(v[8 * q + 2]) * inv_l, __uint_as_float(v[8 * q + 3]) * inv_l),
+                              pack_bf16(__uint_as_float(v[8 * q + 4]) * inv_l, __uint_as_float(v[8 * q + 5]) * inv_l),
+                              pack_bf16(__uint_as_float(v[8 * q + 6]) * inv_l, __uint_as_float(v[8 * q + 7]) * inv_l));
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's smem / TMEM are read by the leader's MMAs until o_done
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2cta(tmem_base, 512);
+  }
+  if (threadIdx.x == 0) p.flags[blockIdx.x] = *win_flag;
+}
+
 // Merge the KV-range partials of the split units in piece order:
 // O = sum_s 2^(m_s - m) O_s / sum_s 2^(m_s - m) l_s (one warp per query row).
 __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnParams p) {
@@ -701,6 +1052,7 @@ int preload_attn_tc() {
   cudaFuncAttributes a;
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_tc_kernel<true>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_tc_kernel<false>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_tc2_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_combine_kernel));
   return LP_OK;
 }
@@ -730,11 +1082,15 @@ static double makespan(const std::vector<double>& costs, int sms) {
   return end;
 }
 
-static AttnPlan plan_attention(int n_q, int n_heads, int sms) {
+// `slots` = concurrent work units (SMs, or SM pairs for the cluster-pair
+// kernel); c_rag = relative cost of a unit whose second 128-row tile is empty
+// (0.6 single-CTA: its MMAs and softmax are skipped; 1.0 for a pair, whose
+// M = 256 MMAs run regardless).
+static AttnPlan plan_attention(int n_q, int n_heads, int sms, double c_rag = 0.6) {
   static std::mutex mu;
-  static std::map<std::tuple<int, int, int>, AttnPlan> cache;
+  static std::map<std::tuple<int, int, int, int>, AttnPlan> cache;
   std::lock_guard<std::mutex> lock(mu);
-  auto key = std::make_tuple(n_q, n_heads, sms);
+  auto key = std::make_tuple(n_q, n_heads, sms, (int)(c_rag * 100));
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   AttnPlan pl;
@@ -743,7 +1099,7 @@ static AttnPlan plan_attention(int n_q, int n_heads, int sms) {
   pl.reg_pairs = pl.pairs - (ragged ? 1 : 0);
   pl.n_units = pl.pairs * n_heads;
   const int n_reg = pl.reg_pairs * n_heads;
-  const double c_rag = 0.6, eps = 0.02;
+  const double eps = 0.02;
   auto cost = [&](int u) { return u < n_reg ? 1.0 : c_rag; };
   double best = 1e300;
   AttnPlan bp = pl;
@@ -776,10 +1132,12 @@ static AttnPlan plan_attention(int n_q, int n_heads, int sms) {
 static int64_t partial_bytes(const AttnPlan& pl) { return pl.pieces() * (2 * AT_M) * (AT_D + 2) * 4; }
 static int64_t flag_bytes(int grid) { return ((int64_t)grid * 4 + 255) / 256 * 256; }
 
+static AttnPlan plan_pair(int n_q, int n_heads) { return plan_attention(n_q, n_heads, num_sms() / 2, 1.0); }
+
 int64_t attention_workspace_bytes(int n_q, int n_heads) {
   if (n_q <= 0 || n_heads <= 0 || num_sms() <= 0) return 0;
-  const AttnPlan pl = plan_attention(n_q, n_heads, num_sms());
-  return partial_bytes(pl) + flag_bytes(pl.grid());
+  const AttnPlan p1 = plan_attention(n_q, n_heads, num_sms()), p2 = plan_pair(n_q, n_heads);
+  return std::max(partial_bytes(p1), partial_bytes(p2)) + flag_bytes(2 * std::max(p1.grid(), p2.grid()));
 }
 
 int attention_tc(const lp_attn_args* a, cudaStream_t st) {
@@ -794,14 +1152,19 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
   if (rc) return rc;
   rc = make_tmap_bf16_2d(&tv, a->v_arena, (uint64_t)a->arena_rows, (uint64_t)d, (uint64_t)d, AT_N, 64);
   if (rc) return rc;
-  AttnPlan pl = plan_attention(a->n_q, a->n_heads, num_sms());
+  // cluster-pair kernel (default) or the single-CTA one (LP_ATTN_SINGLE=1, A/B)
+  const bool pair_k = getenv("LP_ATTN_SINGLE") == nullptr && getenv("LP_ATTN_EXACT") == nullptr;
+  AttnPlan pl = pair_k ? plan_pair(a->n_q, a->n_heads) : plan_attention(a->n_q, a->n_heads, num_sms());
   const int64_t have = a->workspace ? a->workspace_bytes : 0;
-  if (pl.pieces() > 0 && have < partial_bytes(pl) + flag_bytes(pl.grid())) {
+  const int fl_words = (pair_k ? 2 : 1) * pl.grid();
+  if (pl.pieces() > 0 && have < partial_bytes(pl) + flag_bytes(fl_words)) {
     pl.n_whole = pl.n_units;  // no (or too small a) workspace: run every unit whole
     pl.split = 1;
   }
-  // the bounded-exponent kernel needs the flag words (after the partials)
-  const bool fast = have >= partial_bytes(pl) + flag_bytes(pl.grid()) && getenv("LP_ATTN_EXACT") == nullptr;
+  // the bounded-exponent kernels need the flag words (after the partials);
+  // without them the exact single-CTA kernel runs every unit
+  const bool fast = have >= partial_bytes(pl) + flag_bytes((pair_k ? 2 : 1) * pl.grid()) &&
+                    getenv("LP_ATTN_EXACT") == nullptr;
   AttnParams p;
   p.n_q = a->n_q;
   p.n_heads = a->n_heads;
@@ -816,8 +1179,18 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
   p.part_o = static_cast<float*>(a->workspace);
   p.part_ml = p.part_o ? p.part_o + pl.pieces() * (2 * AT_M) * AT_D : nullptr;
   p.flags = fast ? reinterpret_cast<int*>(static_cast<char*>(a->workspace) + partial_bytes(pl)) : nullptr;
+  p.flag_pairs = fast && pair_k;
   const int smem = AttnSmem::TOTAL;
-  if (fast) {
+  if (fast && pair_k) {
+    CUtensorMap tk2;  // this CTA's 64 keys of a tile
+    rc = make_tmap_bf16_2d(&tk2, a->k_arena, (uint64_t)a->arena_rows, (uint64_t)d, (uint64_t)d, 64, 64);
+    if (rc) return rc;
+    LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Attn2Smem::TOTAL));
+    attn_tc2_kernel<<<2 * pl.grid(), AT_THREADS, Attn2Smem::TOTAL, st>>>(tq, tk2, tv, p);
+    rc = launch_status("attention_tc2");
+    if (rc) return rc;
+  } else if (fast) {
     LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attn_tc_kernel<true><<<pl.grid(), AT_THREADS, smem, st>>>(tq, tk, tv, p);
     rc = launch_status("attention_tc_window");

@@ -140,61 +140,6 @@ __global__ void __launch_bounds__(THREADS) norm_mod_kernel(const float* __restri
   }
 }
 
-// One WARP per row (bf16 output, the product path): the row stays in
-// registers (NV float4 per lane, 32 consecutive float4 per warp load), both
-// moments are warp-shuffle reductions -- no shared memory, no CTA barrier --
-// and 8 rows per 256-thread CTA keep ~160 KB of loads in flight per SM.
-template <int NV>
-__global__ void __launch_bounds__(256) norm_mod_warp_kernel(const float* __restrict__ h, int rows, int d, int mode,
-                                                            float eps, const float* __restrict__ shift,
-                                                            const float* __restrict__ scale,
-                                                            __nv_bfloat16* __restrict__ out) {
-  const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (row >= rows) return;
-  const float4* x = reinterpret_cast<const float4*>(h + (int64_t)row * d);
-  const int n4 = d / 4;
-  float4 v[NV];
-  float s = 0.0f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int c = i * 32 + lane;
-    v[i] = c < n4 ? x[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  const float mu = s / d;
-  float q = 0.0f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    if (i * 32 + lane < n4) {
-      const float a = v[i].x - mu, b = v[i].y - mu, e = v[i].z - mu, f = v[i].w - mu;
-      q += (a * a + b * b) + (e * e + f * f);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-  const float rstd = rsqrtf(q / d + eps);
-  uint2* o2 = reinterpret_cast<uint2*>(out + (int64_t)row * d);
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int c = i * 32 + lane;
-    if (c >= n4) continue;
-    float y[4] = {(v[i].x - mu) * rstd, (v[i].y - mu) * rstd, (v[i].z - mu) * rstd, (v[i].w - mu) * rstd};
-    if (mode == 2) {
-      const float4 sc = __ldg(reinterpret_cast<const float4*>(scale) + c);
-      const float4 sh = __ldg(reinterpret_cast<const float4*>(shift) + c);
-      y[0] = y[0] * (1.0f + sc.x) + sh.x;
-      y[1] = y[1] * (1.0f + sc.y) + sh.y;
-      y[2] = y[2] * (1.0f + sc.z) + sh.z;
-      y[3] = y[3] * (1.0f + sc.w) + sh.w;
-    }
-    __nv_bfloat162 p0 = __floats2bfloat162_rn(y[0], y[1]);
-    __nv_bfloat162 p1 = __floats2bfloat162_rn(y[2], y[3]);
-    o2[c] = make_uint2(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1));
-  }
-}
-
 // ----------------------------------------------------------- sink refresh --
 // One warp per (sink token, head): optional RMSNorm(k) then rotation at the
 // sink position i + delta (kvcache.py:86-90, denoiser.py:249); v copied.
@@ -506,9 +451,6 @@ int preload_rows() {
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<__nv_bfloat16, 256>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<__nv_bfloat16, 128, 10>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<float, 128, 10>));
-  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_warp_kernel<12>));
-  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_warp_kernel<24>));
-  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_warp_kernel<40>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, sink_refresh_kernel<float>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, sink_refresh_kernel<__nv_bfloat16>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, sink_refresh_t_kernel<float>));
@@ -542,18 +484,6 @@ int norm_mod(const float* h, int rows, int d, int mode, float eps, const float* 
   LP_CHECK_ARG(mode == 0 || d % 4 == 0, "norm_mod: d must be a multiple of 4");
   LP_CHECK_ARG(mode != 2 || (shift && scale), "norm_mod: modulation needs shift and scale");
   if (rows == 0) return LP_OK;
-  if (mode != 0 && out_dtype == LP_BF16 && d % 128 == 0 && d <= 128 * 40 && getenv("LP_NORM_CTA") == nullptr) {
-    // product path: one warp per row (d = 1536 -> 12, d = 5120 -> 40 float4 per lane)
-    const int blocks = (rows + 7) / 8;
-    auto* o = (__nv_bfloat16*)out;
-    if (d <= 128 * 12)
-      norm_mod_warp_kernel<12><<<blocks, 256, 0, st>>>(h, rows, d, mode, eps, shift, scale, o);
-    else if (d <= 128 * 24)
-      norm_mod_warp_kernel<24><<<blocks, 256, 0, st>>>(h, rows, d, mode, eps, shift, scale, o);
-    else
-      norm_mod_warp_kernel<40><<<blocks, 256, 0, st>>>(h, rows, d, mode, eps, shift, scale, o);
-    return launch_status("norm_mod");
-  }
   if (d <= 2048) {  // narrow rows (1.3B: d = 1536): 128 threads, 4 float4 per thread
     if (out_dtype == LP_BF16)
       norm_mod_kernel<__nv_bfloat16, 128, 4><<<rows, 128, 0, st>>>(h, d, mode, eps, shift, scale,
