@@ -685,14 +685,17 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 // so S(j+2) is issued as soon as the softmax has LOADED S(j) (s_free), before
 // its exponentials: the tensor core runs S(j+2) while softmax(j) computes and
 // PV(j) once P(j) is stored.  Nothing on the tensor pipe waits on the softmax
-// latency, only on its throughput.  Two softmax warpgroups per CTA split the
-// 128 keys of a tile (64 each, all 128 rows by TMEM lane quarter): with the
-// bounded-exponent offset (max of the first tile, exchanged once) they never
+// latency, only on its throughput.  Two softmax warpgroups per CTA take the
+// KV tiles alternately (S_b / P_b belong to warpgroup b), so the two warps
+// sharing an SM sub-partition are half a tile out of phase and hide each
+// other's TMEM-load and barrier latency; with the bounded-exponent offset
+// (max of tile 0, handed to warpgroup 1 once) they share one offset and never
 // synchronise per tile; their row sums are added at the end.
 //   warp 0      TMA producer (both CTAs): Q once, K/V halves (4-stage rings),
 //               completion counted on the leader's barriers
-//   warp 1      TMEM allocation (both), MMA issue (leader only)
-//   warps 4-7   softmax keys [0, 64)    warps 8-11  softmax keys [64, 128)
+//   warp 1      TMEM allocation (both); leader: issues the S = Q K^T MMAs
+//   warp 2      leader: issues the O += P V MMAs
+//   warps 4-7   softmax of tiles 0, 2, 4, ...    warps 8-11  tiles 1, 3, 5, ...
 constexpr int A2_KS = 4, A2_VS = 4;          // K / V ring stages
 constexpr int A2_KT = 64 * AT_D * 2;         // 16 KB: this CTA's 64 keys x 128 dims
 constexpr int A2_KHALF = 64 * 64 * 2;        // 8 KB: one 64-dim SW128 block of it
@@ -722,10 +725,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
   uint64_t* v_full = k_empty + A2_KS;    // [VS] leader
   uint64_t* v_empty = v_full + A2_VS;    // [VS] both
   uint64_t* s_full = v_empty + A2_VS;    // [2] both
-  uint64_t* s_free = s_full + 2;         // [2] leader: 8 softmax warps x 2 CTAs loaded S
-  uint64_t* p_lo = s_free + 2;           // [2] leader: keys [0,64) of P stored (4 warps x 2 CTAs)
-  uint64_t* p_hi = p_lo + 2;             // [2] leader: keys [64,128)
-  uint64_t* pv_done = p_hi + 2;          // [2] both: P buffer consumed
+  uint64_t* s_free = s_full + 2;         // [2] leader: warpgroup b's 4 warps x 2 CTAs loaded S_b
+  uint64_t* p_lo = s_free + 2;           // [2] leader: P(j) of buffer j&1 stored (4 warps x 2 CTAs)
+  uint64_t* pv_done = p_lo + 2;          // [2] both: P buffer consumed
   uint64_t* o_done = pv_done + 2;        // both
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
   float* xch = reinterpret_cast<float*>(smem + Attn2Smem::XCH_OFF);  // [2][128] per-row exchange
@@ -768,9 +770,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 16);
+      mbar_init(&s_free[i], 8);
       mbar_init(&p_lo[i], 8);
-      mbar_init(&p_hi[i], 8);
       mbar_init(&pv_done[i], 1);
     }
     mbar_init(o_done, 1);
@@ -812,56 +813,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
                         cur.cur_row(), pol);
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer (leader)
-    if (rank == 0) {
-      constexpr uint32_t IDESC_S = idesc_bf16_f32(2 * AT_M, AT_N);               // Q K^T, both K-major
-      constexpr uint32_t IDESC_O = idesc_bf16_f32(2 * AT_M, AT_D, false, true);  // P V: P in TMEM, V MN-major
+  } else if ((warp == 1 || warp == 2) && rank == 0) {
+    // ------------------------------------------------ MMA issue (leader), two
+    // independent in-order streams so neither waits behind the other's
+    // dependency: warp 1 issues S(t) as soon as S_{t&1} is free (softmax(t-2)
+    // has loaded it) and K_t has landed; warp 2 issues PV(j) as soon as P(j)
+    // is stored.  O is only written by warp 2's stream (in order); S and P
+    // live in separate TMEM columns.
+    constexpr uint32_t IDESC_S = idesc_bf16_f32(2 * AT_M, AT_N);               // Q K^T, both K-major
+    constexpr uint32_t IDESC_O = idesc_bf16_f32(2 * AT_M, AT_D, false, true);  // P V: P in TMEM, V MN-major
+    if (warp == 1) {
       const uint32_t sq = smem_u32(smem + Attn2Smem::Q_OFF);
-      auto issue_s = [&](int t) {  // S_{t&1} = Q K_t^T
-        const uint32_t sk = smem_u32(smem + Attn2Smem::K_OFF + (t % A2_KS) * A2_KT);
-#pragma unroll
-        for (int kk = 0; kk < AT_D / 16; ++kk)
-          mma_bf16_ss_2cta(tmem_base + (t & 1) * AT_N,
-                           sdesc_kmajor_sw128(sq + (kk >> 2) * AT_HALF + (kk & 3) * 32),
-                           sdesc_kmajor_sw128(sk + (kk >> 2) * A2_KHALF + (kk & 3) * 32), IDESC_S, kk != 0);
-        mma_commit_2cta_mc(&s_full[t & 1]);
-        mma_commit_2cta_mc(&k_empty[t % A2_KS]);
-      };
-      auto issue_pv = [&](int t, int h) {  // O += P_{t&1}[keys 64h..] V_t[64h..]
-        const uint32_t sv = smem_u32(smem + Attn2Smem::V_OFF + (t % A2_VS) * A2_VT);
-        const uint32_t tp = tmem_base + 384 + (t & 1) * 64;
-#pragma unroll
-        for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
-          mma_bf16_ts_2cta(tmem_base + 256, tp + kk * 8, sdesc_mnmajor_sw128(sv + kk * 16 * 128, A2_VT), IDESC_O,
-                           (t | kk) != 0);
-      };
       mbar_wait(q_full, 0);
-      for (int t = 0; t < min(2, n_tiles); ++t) {
+      for (int t = 0; t < n_tiles; ++t) {
+        if (t >= 2) mbar_wait(&s_free[t & 1], ((t - 2) >> 1) & 1);
         mbar_wait(&k_full[t % A2_KS], (t / A2_KS) & 1);
         tc_fence_after();
-        if (elect_one()) issue_s(t);
+        if (elect_one()) {
+          const uint32_t sk = smem_u32(smem + Attn2Smem::K_OFF + (t % A2_KS) * A2_KT);
+#pragma unroll
+          for (int kk = 0; kk < AT_D / 16; ++kk)
+            mma_bf16_ss_2cta(tmem_base + (t & 1) * AT_N,
+                             sdesc_kmajor_sw128(sq + (kk >> 2) * AT_HALF + (kk & 3) * 32),
+                             sdesc_kmajor_sw128(sk + (kk >> 2) * A2_KHALF + (kk & 3) * 32), IDESC_S, kk != 0);
+          mma_commit_2cta_mc(&s_full[t & 1]);
+          mma_commit_2cta_mc(&k_empty[t % A2_KS]);
+        }
         __syncwarp();
       }
+    } else {
       for (int j = 0; j < n_tiles; ++j) {
         const int b = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        if (j + 2 < n_tiles) {  // S(j+2) into S_b as soon as softmax(j) has loaded S(j)
-          mbar_wait(&s_free[b], ph);
-          mbar_wait(&k_full[(j + 2) % A2_KS], ((j + 2) / A2_KS) & 1);
-          tc_fence_after();
-          if (elect_one()) issue_s(j + 2);
-          __syncwarp();
-        }
         mbar_wait(&v_full[j % A2_VS], (j / A2_VS) & 1);
-        mbar_wait(&p_lo[b], ph);
-        tc_fence_after();
-        if (elect_one()) issue_pv(j, 0);
-        __syncwarp();
-        mbar_wait(&p_hi[b], ph);
+        mbar_wait(&p_lo[b], (j >> 1) & 1);  // P(j) stored by warpgroup b (both CTAs)
         tc_fence_after();
         if (elect_one()) {
-          issue_pv(j, 1);
+          const uint32_t sv = smem_u32(smem + Attn2Smem::V_OFF + (j % A2_VS) * A2_VT);
+          const uint32_t tp = tmem_base + 384 + b * 64;
+#pragma unroll
+          for (int kk = 0; kk < AT_N / 16; ++kk)
+            mma_bf16_ts_2cta(tmem_base + 256, tp + kk * 8, sdesc_mnmajor_sw128(sv + kk * 16 * 128, A2_VT), IDESC_O,
+                             (j | kk) != 0);
           mma_commit_2cta_mc(&pv_done[b]);
           mma_commit_2cta_mc(&v_empty[j % A2_VS]);
         }
@@ -873,60 +865,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------ softmax (both CTAs)
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(AT_REG_SOFTMAX));
-    const int w = (warp - 4) / 4;        // key half of every tile
+    const int x = (warp - 4) / 4;        // this warpgroup's tiles: j = x, x + 2, ...
+    const int w = x;                     // (epilogue: output column half)
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;   // row within this CTA's 128 == TMEM lane
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const uint32_t t_s = tmem_base + lane_base + 64 * w;
-    const uint32_t t_p = tmem_base + lane_base + 384 + 32 * w;
+    const uint32_t t_s = tmem_base + lane_base + x * AT_N;
+    const uint32_t t_p = tmem_base + lane_base + 384 + x * 64;
     const uint32_t t_o = tmem_base + lane_base + 256;
     const float sc = p.scale_log2;
     float m_run = 0.0f, l_run = 0.0f;
     uint64_t wa2 = 0, wb2 = 0, sc2 = f32x2(sc, sc), nm2 = 0;
+    auto set_offset = [&](float m) {
+      m_run = m;
+      const float wa = sc * (1.0f / 192.0f), wb = (127.0f - m_run) * (1.0f / 192.0f);
+      wa2 = f32x2(wa, wa);
+      wb2 = f32x2(wb, wb);
+      nm2 = f32x2(-m_run, -m_run);
+    };
+    // the shared exponent offset (max of tile 0) reaches warpgroup 1 once
+    if (x == 1 && n_tiles > 0) {
+      softmax_bar();
+      set_offset(xch[r]);
+    }
     TileCursor cs;
     cs.init(seg_row, seg_len, n_seg_s[0]);
-    cs.skip(t_first);
-    for (int j = 0; j < n_tiles; ++j, cs.next()) {
-      const int b = j & 1;
+    cs.skip(t_first + x);
+    for (int j = x; j < n_tiles; j += 2, cs.next(), cs.next()) {
       const uint32_t ph = (j >> 1) & 1;
-      const int nvalid = cs.cur_valid() - 64 * w;  // valid keys of this warp's half
-      mbar_wait(&s_full[b], ph);
+      const int nvalid = cs.cur_valid();
+      mbar_wait(&s_full[x], ph);
       tc_fence_after();
-      uint32_t s[64];
-      tmem_ld32(t_s + b * AT_N, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-      tmem_ld32(t_s + b * AT_N + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+      uint32_t s[128];
+      tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+      tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+      tmem_ld32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
+      tmem_ld32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_remote(&s_free[b], 0);
-      if (nvalid < 64) {  // ragged segment tail (warp-uniform)
+      if (lane == 0) mbar_arrive_remote(&s_free[x], 0);  // S_x may take S(j+2)
+      if (nvalid < AT_N) {  // ragged segment tail (warp-uniform)
 #pragma unroll
-        for (int i = 0; i < 64; ++i)
+        for (int i = 0; i < 128; ++i)
           if (i >= nvalid) s[i] = __float_as_uint(-INFINITY);
       }
-      if (j == 0) {  // the row's exponent offset: max of the first tile, both key halves
+      if (j == 0) {  // tile 0: the row's exponent offset for the whole unit
         float mq[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) mq[k] = __uint_as_float(s[k]);
+        for (int k = 0; k < 8; ++k) mq[k] = fmaxf(__uint_as_float(s[k]), __uint_as_float(s[k + 8]));
 #pragma unroll
-        for (int i = 8; i < 64; i += 8)
+        for (int i = 16; i < 128; i += 16)
 #pragma unroll
-          for (int k = 0; k < 8; ++k) mq[k] = fmaxf(mq[k], __uint_as_float(s[i + k]));
-        xch[w * AT_M + r] = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
-                                  fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
+          for (int k = 0; k < 8; ++k)
+            mq[k] = fmaxf(mq[k], fmaxf(__uint_as_float(s[i + k]), __uint_as_float(s[i + 8 + k])));
+        const float mx = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
+                               fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7]))) * sc;
+        xch[r] = mx;
         softmax_bar();
-        m_run = fmaxf(xch[r], xch[AT_M + r]) * sc;
-        const float wa = sc * (1.0f / 192.0f), wb = (127.0f - m_run) * (1.0f / 192.0f);
-        wa2 = f32x2(wa, wa);
-        wb2 = f32x2(wb, wb);
-        nm2 = f32x2(-m_run, -m_run);
+        set_offset(mx);
       }
-      if (j >= 2) mbar_wait(&pv_done[b], ph ^ 1);  // P_b of tile j-2 consumed
       uint64_t rs2[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) rs2[k] = f32x2(0.f, 0.f);
 #pragma unroll
-      for (int i = 0; i < 64; i += 2) {
+      for (int i = 0; i < 128; i += 2) {
         const bool poly = ((i >> 1) & 7) >= 8 - LP_ATTN_POLY_WIN;
         const uint64_t sv2 = f32x2(__uint_as_float(s[i]), __uint_as_float(s[i + 1]));
         uint64_t e;
@@ -943,17 +946,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
         unpack_f32x2(e, e0, e1);
         s[i / 2] = pack_bf16(e0, e1);
       }
-      tmem_st32_x(t_p + b * 64, &s[0]);
+      if (j >= 2) {  // P_x of tile j-2 consumed (the exps above did not wait for it)
+        mbar_wait(&pv_done[x], ph ^ 1);
+        tc_fence_after();
+      }
+      tmem_st32_x(t_p, &s[0]);
+      tmem_st32_x(t_p + 32, &s[32]);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_remote(w == 0 ? &p_lo[b] : &p_hi[b], 0);
+      if (lane == 0) mbar_arrive_remote(&p_lo[x], 0);
       float rr[8];
 #pragma unroll
       for (int k = 0; k < 4; ++k) unpack_f32x2(rs2[k], rr[2 * k], rr[2 * k + 1]);
       l_run += ((rr[0] + rr[1]) + (rr[2] + rr[3])) + ((rr[4] + rr[5]) + (rr[6] + rr[7]));
     }
-    // epilogue: the row sum of both key halves, then O / l (or partials);
+    // epilogue: the row sums of both warpgroups' tiles, then O / l (or partials);
     // each warpgroup stores 64 of the 128 output columns of its rows
     mbar_wait(o_done, 0);
     tc_fence_after();
