@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LP_ABI_VERSION 3
+#define LP_ABI_VERSION 4
 
 /* status codes */
 #define LP_OK 0
@@ -271,6 +271,15 @@ LP_API int lp_patchify(const float* x, int frames, int c, int h, int w, int ph, 
 LP_API int lp_unpatchify_euler(const float* x, const float* v_tokens, int frames, int c,
                         int h, int w, int ph, int pw, const lp_block_desc* desc,
                         float* x_out, void* stream);
+
+/* The reference's analytic test denoiser fused with the flow step
+   (OracleDenoiser.denoise_block, denoiser.py:294-343 + flow_step,
+   latent.py:140-147): vel = (x - target) / s (written when vel != NULL),
+   x_out = x + vel * dt; IEEE fp32 in the reference's operation order, so the
+   result is bitwise the reference's.  s == 0 -> LP_EINVAL (the reference
+   raises ValueError "oracle velocity undefined at s = 0").                 */
+LP_API int lp_oracle_step(const float* x, const float* target, float s, float dt, float* vel, float* x_out,
+                          int64_t n, void* stream);
 
 /* History noise (kvcache.py:121-137) for one layer and one of K/V (kv 0/1):
    for every history segment s in [1, n_seg-1) of desc, arena rows

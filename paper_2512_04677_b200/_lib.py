@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LIVEPIPE_LIB") or os.path.join(HERE, "liblivepipe_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "livepipe_b200.h")
 
-ABI_VERSION = 3  # LP_ABI_VERSION in include/livepipe_b200.h
+ABI_VERSION = 4  # LP_ABI_VERSION in include/livepipe_b200.h
 LP_OK, LP_EINVAL, LP_ECUDA, LP_EUNSUPPORTED, LP_ETIMEOUT, LP_EABORT = range(6)
 LP_F32, LP_BF16 = 0, 1
 EPI_STORE, EPI_RELU, EPI_GELU, EPI_RESID, EPI_QKV, EPI_EULER = range(6)
@@ -89,6 +89,7 @@ _SIGS = {
                                   C.c_int, C.c_int, i64, i64, vp], C.c_int),
     "lp_silu": ([vp, vp, C.c_int, C.c_int, vp], C.c_int),
     "lp_patchify": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
+    "lp_oracle_step": ([vp, vp, C.c_float, C.c_float, vp, vp, i64, vp], C.c_int),
     "lp_unpatchify_euler": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp],
                             C.c_int),
     "lp_fork_create": ([C.POINTER(vp)], C.c_int),

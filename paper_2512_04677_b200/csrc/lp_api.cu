@@ -38,6 +38,7 @@ int patchify(const float*, int, int, int, int, int, int, void*, int, cudaStream_
 int unpatchify_euler(const float*, const float*, int, int, int, int, int, int, const lp_block_desc*, float*,
                      cudaStream_t);
 int history_noise(void*, int, int, const float*, int, int, int, const lp_block_desc*, int, cudaStream_t);
+int oracle_step(const float*, const float*, float, float, float*, float*, int64_t, cudaStream_t);
 int randn(void*, int64_t, uint64_t, uint64_t, float, int, cudaStream_t);
 int link_send(const void*, void*, int64_t, volatile uint32_t*, const volatile uint32_t*, uint32_t, int,
               const volatile uint32_t*, uint64_t, int32_t*, cudaStream_t);
@@ -182,6 +183,11 @@ int lp_patchify(const float* x, int frames, int c, int h, int w, int ph, int pw,
 int lp_unpatchify_euler(const float* x, const float* v_tokens, int frames, int c, int h, int w, int ph, int pw,
                         const lp_block_desc* desc, float* x_out, void* stream) {
   return unpatchify_euler(x, v_tokens, frames, c, h, w, ph, pw, desc, x_out, S(stream));
+}
+
+int lp_oracle_step(const float* x, const float* target, float s, float dt, float* vel, float* x_out, int64_t n,
+                   void* stream) {
+  return oracle_step(x, target, s, dt, vel, x_out, n, S(stream));
 }
 
 int lp_history_noise(void* arena, int dtype, int d, const float* noise, int n_layers, int layer, int kv,

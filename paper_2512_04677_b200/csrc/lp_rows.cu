@@ -5,6 +5,9 @@
 
 namespace lp {
 
+__global__ void oracle_step_kernel(const float* __restrict__, const float* __restrict__, float, float,
+                                   float* __restrict__, float* __restrict__, int64_t);
+
 // ------------------------------------------------------------ cond row -----
 // c[col] = a.Wa[:,col] ; c += p.Wp[:,col] ; c += tau.Wt[:,col]
 // (denoiser.py:178-185: three pinned-order products summed in this order).
@@ -451,6 +454,7 @@ int preload_rows() {
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<__nv_bfloat16, 256>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<__nv_bfloat16, 128, 10>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<float, 128, 10>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, oracle_step_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, sink_refresh_kernel<float>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, sink_refresh_kernel<__nv_bfloat16>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, sink_refresh_t_kernel<float>));
@@ -566,6 +570,27 @@ int patchify(const float* x, int frames, int C, int H, int W, int ph, int pw, vo
   else
     patchify_kernel<float><<<nblk(n, 256), 256, 0, st>>>(x, frames, C, H, W, ph, pw, (float*)tok);
   return launch_status("patchify");
+}
+
+// The reference's analytic test denoiser (OracleDenoiser, denoiser.py:294-343)
+// fused with the flow step (latent.py:140-147):
+//   v = (x - target) / s ;  x' = x + v * dt   -- IEEE ops in numpy's order, no FMA.
+__global__ void oracle_step_kernel(const float* __restrict__ x, const float* __restrict__ target, float s, float dt,
+                                   float* __restrict__ vel, float* __restrict__ x_out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float v = __fdiv_rn(__fsub_rn(x[i], target[i]), s);
+  if (vel) vel[i] = v;
+  x_out[i] = __fadd_rn(x[i], __fmul_rn(v, dt));
+}
+
+int oracle_step(const float* x, const float* target, float s, float dt, float* vel, float* x_out, int64_t n,
+                cudaStream_t st) {
+  LP_CHECK_ARG(x && target && x_out, "lp_oracle_step: null pointer");
+  LP_CHECK_ARG(s != 0.0f, "lp_oracle_step: oracle velocity undefined at s = 0");
+  if (n <= 0) return LP_OK;
+  oracle_step_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, target, s, dt, vel, x_out, n);
+  return launch_status("oracle_step");
 }
 
 int unpatchify_euler(const float* x, const float* v, int frames, int C, int H, int W, int ph, int pw,

@@ -48,6 +48,7 @@ THREADS_ENV = "LIVE_PIPE_THREADS"
 ORACLE_TARGET_STREAM = 1 << 46
 MODES = ("sequential", "clean_kv", "tpp", "simulate")
 DENOISER_KINDS = ("toy", "oracle")
+ORACLE_TARGET_STREAM = 1 << 46  # Philox stream of the oracle denoiser's target (reference engine.py:59)
 PRECISIONS = ("fp32", "bf16")
 
 
@@ -102,12 +103,11 @@ class EngineConfig:
             raise EngineConfigError(f"mode must be one of {MODES}, got {self.mode!r}")
         if self.denoiser_kind not in DENOISER_KINDS:
             raise EngineConfigError(f"denoiser must be one of {DENOISER_KINDS}")
-        if self.denoiser_kind == "oracle":
-            # the reference's analytic (x - target)/s test denoiser
-            # (denoiser.py:294-343) has no DiT math to accelerate; refusing is
-            # louder than silently running the toy model in its place
-            raise EngineConfigError("denoiser_kind='oracle' is the reference's analytic test denoiser and is not "
-                                    "part of the B200 path; run it on the reference engine")
+        if self.denoiser_kind == "oracle" and self.profile is not None and self.profile.patched:
+            # the reference's analytic test denoiser (denoiser.py:294-343) is
+            # defined over the toy model's per-frame K/V projections
+            raise EngineConfigError("denoiser_kind='oracle' needs the toy profile (the reference's analytic "
+                                    "test denoiser projects K/V per latent frame)")
         if (self.profile is not None and self.rope_base != 10000.0
                 and self.rope_base != self.profile.rope_base):
             raise EngineConfigError(f"rope_base {self.rope_base} disagrees with the profile's "
@@ -181,6 +181,9 @@ class Runtime:
     device_codecs: dict = field(default_factory=dict)  # device index -> codec.DeviceCodec
     weight_seed: int | None = None  # host weights rebuilt on demand from (seed, profile)
     profile: ModelProfile | None = None
+    # denoiser_kind='oracle': the analytic velocity's target block
+    # (engine.py:191-197, Philox(oracle_target_seed, 1<<46))
+    oracle_target: np.ndarray | None = None
 
     @property
     def weights(self) -> DenoiserWeights | None:
@@ -216,7 +219,10 @@ def build_runtime(cfg: EngineConfig) -> Runtime:
         codec = PatchVideoCodec(cfg.weight_seed, prof.channels, prof.height, prof.width, cfg.pixel_channels,
                                 cfg.pixel_scale, cfg.upsample)
     conds = synthetic_conditions(cfg.noise_seed, cfg.blocks, prof.audio_dim, prof.prompt_dim, prof.latent_dim)
-    return Runtime(schedule, None, dws, codec, conds, weight_seed=seed, profile=prof)
+    target = None
+    if cfg.denoiser_kind == "oracle":
+        target = Prng(cfg.oracle_target_seed, ORACLE_TARGET_STREAM).normal((cfg.frames_per_block, prof.latent_dim))
+    return Runtime(schedule, None, dws, codec, conds, weight_seed=seed, profile=prof, oracle_target=target)
 
 
 def noise_block(cfg: EngineConfig, block_index: int) -> LatentBlock:
@@ -249,6 +255,8 @@ class Stage:
                                  f"cuda:{device}")
             self.fw = Forward(dw, cfg.frames_per_block, self.arena)
             self.fw.sink_v_static = True  # sink rows fixed at [0, S) (write_inputs sink_row=0)
+            if rt.oracle_target is not None:  # analytic velocity + the per-frame K/V projections
+                self.fw.set_oracle(rt.oracle_target, rt.schedule.level(j), rt.schedule.dt)
         self.fw.set_history_noise(self.sigma_on, None)
         self._noise_host = self._noise_dev = self._noise_ev = None
         if self.sigma_on and not cfg.device_inputs:
@@ -712,6 +720,9 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
 def run_clean_kv(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
     if cfg.mode != "clean_kv":
         raise EngineConfigError(f"run_clean_kv called with mode {cfg.mode!r}")
+    if cfg.denoiser_kind != "toy":
+        raise EngineConfigError("clean_kv runs the toy denoiser through the drop-in; the oracle kind's clean-KV "
+                                "baseline runs on the reference engine")
     rt = rt or build_runtime(cfg)
     if rt.weights is None:
         raise EngineConfigError("clean_kv needs host weights (device_inputs=False)")

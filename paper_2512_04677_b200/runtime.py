@@ -436,6 +436,9 @@ class Forward:
         ldt = dw.ldt
         xo = self.x_out if x_out is None else x_out
         xo_ptr = xo if isinstance(xo, int) else xo.data_ptr()  # an int is a (peer-mapped) device address
+        if self.oracle is not None:
+            self._launch_oracle(st, xo_ptr)
+            return
         # conditioning row (denoiser.py:178-185)
         L.call("lp_cond_row", self.audio_ptr if self.audio_present else None, prof.audio_dim,
                dw.w_audio.data_ptr(), self.prompt_ptr, prof.prompt_dim, dw.w_prompt.data_ptr(), self.tau_ptr, 8,
@@ -558,6 +561,40 @@ class Forward:
             args.a, args.w, args.c = self.xa.data_ptr(), dw.w_vel.data_ptr(), 0
             args.euler = C.pointer(self._euler)
             L.call("lp_gemm", C.byref(args), st)
+
+    # denoiser_kind='oracle': (target device tensor, level s, dt) of the
+    # reference's analytic test denoiser (denoiser.py:294-343)
+    oracle = None
+
+    def set_oracle(self, target: np.ndarray, s: float, dt: float) -> None:
+        t = torch.from_numpy(np.ascontiguousarray(target, dtype=np.float32)).to(self.device)
+        self.oracle = (t.reshape(-1), float(F32(s)), float(F32(dt)))
+
+    def _launch_oracle(self, st: int, xo_ptr: int) -> None:
+        """OracleDenoiser.denoise_block + flow_step: the cache entry is the
+        plain per-layer projections x.Wk (rotated at the block index) and
+        x.Wv written into the ring slot (denoiser.py:307-322); the velocity
+        (x - target)/s and the Euler step are one elementwise kernel."""
+        prof, dw, ar = self.prof, self.dw, self.arena
+        N, d = self.n_tokens, prof.model_dim
+        esz = ar.k.element_size()
+        a = self.x_in.data_ptr()
+        if not self.fp32:  # bf16 GEMM operand
+            L.call("lp_norm_mod", self.x_in.data_ptr(), N, d, 0, prof.eps, None, None, self.xa.data_ptr(), dw.ldt, st)
+            a = self.xa.data_ptr()
+        for l in range(prof.n_layers):
+            kl = ar.k.data_ptr() + l * ar.layer_stride * esz
+            vl = ar.v.data_ptr() + l * ar.layer_stride * esz
+            epi = L.QkvEpi(d, prof.n_heads, prof.head_dim, 0, prof.eps, 0, 0, self.q.data_ptr(), kl, vl,
+                           self.desc_ptr, self.geom)
+            if self.fp32:
+                self._proj(st, a, N, d, dw.wqkv[l], 3 * d, self.qkv.data_ptr(), 3 * d, L.EPI_STORE, L.LP_F32)
+                L.call("lp_qkv_post", self.qkv.data_ptr(), N, C.byref(epi), dw.ldt, st)
+            else:
+                self._proj(st, a, N, d, dw.wqkv[l], 3 * d, 0, 0, L.EPI_QKV, qkv=epi)
+        target, s, dt = self.oracle
+        L.call("lp_oracle_step", self.x_in.data_ptr(), target.data_ptr(), s, dt, self.vel.data_ptr(), xo_ptr, N * d,
+               st)
 
     _sigma_on = False
     # device address of a sticky link status word (TPP fused send): the

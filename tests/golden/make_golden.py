@@ -39,6 +39,7 @@ def main() -> None:
         "c1_scaled": dict(steps=4, blocks=5, history_sigma=0.2, history_mode="scaled"),
         "c1_L1": dict(steps=2, blocks=6, cache_capacity=1),
         "c1_delta3": dict(steps=3, blocks=4, sink_delta=3),
+        "c1_oracle": dict(steps=4, blocks=3, denoiser_kind="oracle"),
     }.items():
         seq = lp.run_sequential(lp.EngineConfig(mode="sequential", **kw))
         tpp = lp.run_tpp(lp.EngineConfig(mode="tpp", **kw))

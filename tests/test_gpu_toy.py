@@ -201,3 +201,21 @@ def test_clean_kv_matches_reference(name):
     assert rel_l2(got, G[f"{name}_latents"]) < TOL_FP32
     assert rel_l2(res.frames, G[f"{name}_frames"]) < TOL_FP32
     assert res.nfe == META[name]["nfe"]
+
+
+@pytest.mark.parametrize("mode", ["sequential", "tpp"])
+def test_oracle_denoiser_kind_matches_reference_digest(mode):
+    # denoiser_kind='oracle' (engine.py:191-197, denoiser.py:294-343): the
+    # analytic velocity (x - target)/s fused with the flow step is IEEE fp32
+    # in the reference's operation order -> the reference's latent digest
+    # bit for bit; the K/V projections still go through the ring
+    kw = META["c1_oracle"]["kw"]
+    res = lp.run(lp.EngineConfig(mode=mode, **kw))
+    assert lp.latents_digest(res.blocks) == META["c1_oracle"]["latents_sha256"]
+    assert rel_l2(res.frames, G["c1_oracle_frames"]) < TOL_FP32
+    assert res.nfe == META["c1_oracle"]["nfe"]
+
+
+def test_oracle_denoiser_kind_rejects_wan_profile():
+    with pytest.raises(lp.EngineConfigError):
+        lp.EngineConfig(mode="sequential", denoiser_kind="oracle", profile=lp.WAN_1_3B)
