@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LP_ABI_VERSION 4
+#define LP_ABI_VERSION 5
 
 /* status codes */
 #define LP_OK 0
@@ -151,6 +151,20 @@ typedef struct lp_euler_epi {
                              consumer has not released is never overwritten */
 } lp_euler_epi;
 
+/* Implicit-GEMM convolution over a zero-bordered row layout (the decode
+ * stage's VAE stand-in, codec.py VaeDecoder): A is [rows, cin] bf16 with the
+ * activation stored as [T][H+2][W+2][cin] (one zero pixel of border), and the
+ * GEMM's K = n_taps * cin walks the taps: k-chunk kb reads A rows
+ * m + tap_row[kb / (cin/64)] (TMA zero-fills rows outside [0, m) -- the causal
+ * temporal taps of frame 0), columns (kb % (cin/64)) * 64.  W is
+ * [n, n_taps*cin] (tap-major K).  Output rows are the padded grid; border
+ * rows hold garbage the consumer ignores.                                    */
+typedef struct lp_conv_taps {
+  int32_t n_taps;         /* <= 27                                          */
+  int32_t cin;            /* multiple of 64                                 */
+  int32_t tap_row[27];    /* row offset of each tap in the padded layout    */
+} lp_conv_taps;
+
 typedef struct lp_gemm_args {
   int32_t in_dtype;       /* LP_F32 | LP_BF16                               */
   int32_t out_dtype;      /* for STORE/RELU/GELU                            */
@@ -164,6 +178,8 @@ typedef struct lp_gemm_args {
   const float* gate;      /* [n] or NULL (RESID only)                       */
   const lp_qkv_epi* qkv;  /* host pointer, LP_EPI_QKV only                  */
   const lp_euler_epi* euler; /* host pointer, LP_EPI_EULER only             */
+  const lp_conv_taps* conv; /* host pointer or NULL: implicit-GEMM conv (bf16,
+                             STORE/RESID, single-CTA tiles, no fork)        */
   void* fork;             /* lp_fork_create handle or NULL: lets a bf16 GEMM
                              whose M is not a multiple of 256 run cluster-pair
                              tiles on the whole 256-row blocks and the ragged
@@ -271,6 +287,21 @@ LP_API int lp_patchify(const float* x, int frames, int c, int h, int w, int ph, 
 LP_API int lp_unpatchify_euler(const float* x, const float* v_tokens, int frames, int c,
                         int h, int w, int ph, int pw, const lp_block_desc* desc,
                         float* x_out, void* stream);
+
+/* Decode stage, VAE stand-in (the decode worker engine.py:465-480 runs the
+   reference codec latent.py:150-193; the paper's decode GPU runs the Wan VAE,
+   PAPER.md:186, :304).  Activations are [T][H+2][W+2][C] rows with a
+   one-pixel zero border; the 3-D convolutions are lp_gemm with lp_conv_taps.
+   pack_latent: latent [F, C, H, W] fp32 -> bordered bf16 [F][H+2][W+2][cpad].
+   norm_silu:   fp32 rows -> bf16; mode 1 = RMS norm over C * gamma, SiLU;
+                mode 0 = cast; border pixels written as 0 (C <= 512).
+   upsample:    nearest x2 in H and W, x ft (1|2) in T, bordered bf16 -> bf16.
+   frames:      interior, first cout channels of fp32 rows -> [T][cout][H][W]. */
+LP_API int lp_vae_pack_latent(const float* x, int f, int c, int h, int w, int cpad, void* out, void* stream);
+LP_API int lp_vae_norm_silu(const float* hbuf, const float* gamma, int t, int h, int w, int c, int mode, float eps,
+                            void* out, void* stream);
+LP_API int lp_vae_upsample(const void* in, int t, int h, int w, int c, int ft, void* out, void* stream);
+LP_API int lp_vae_frames(const float* hbuf, int t, int h, int w, int cpad, int cout, float* frames, void* stream);
 
 /* The reference's analytic test denoiser fused with the flow step
    (OracleDenoiser.denoise_block, denoiser.py:294-343 + flow_step,

@@ -26,6 +26,7 @@ from .kvcache import (RollingKvCache, SinkLockedError, SinkSlot, aas_update, cac
 from .latent import (Conditions, LatentBlock, PatchVideoCodec, TimestepSchedule, ToyVideoCodec, flow_step,
                      interpolate, synthetic_conditions, true_velocity)
 from .codec import DeviceCodec
+from .vae import VaeDecoder
 from .metrics import (MetricsBundle, TimelineEvent, compute_fps, compute_ttff, drift_metric,
                       metrics_from_timeline, stage_utilization)
 from .model import (WAN_14B, WAN_1_3B, DenoiserWeights, DeviceWeights, LayerWeights, ModelProfile,

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LIVEPIPE_LIB") or os.path.join(HERE, "liblivepipe_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "livepipe_b200.h")
 
-ABI_VERSION = 4  # LP_ABI_VERSION in include/livepipe_b200.h
+ABI_VERSION = 5  # LP_ABI_VERSION in include/livepipe_b200.h
 LP_OK, LP_EINVAL, LP_ECUDA, LP_EUNSUPPORTED, LP_ETIMEOUT, LP_EABORT = range(6)
 LP_F32, LP_BF16 = 0, 1
 EPI_STORE, EPI_RELU, EPI_GELU, EPI_RESID, EPI_QKV, EPI_EULER = range(6)
@@ -57,11 +57,15 @@ class EulerEpi(C.Structure):
                 ("pw", i32), ("desc", vp), ("gate_status", vp)]
 
 
+class ConvTaps(C.Structure):
+    _fields_ = [("n_taps", i32), ("cin", i32), ("tap_row", i32 * 27)]
+
+
 class GemmArgs(C.Structure):
     _fields_ = [("in_dtype", i32), ("out_dtype", i32), ("epilogue", i32), ("m", i32), ("n", i32),
                 ("k", i32), ("lda", i64), ("ldw", i64), ("ldc", i64), ("a", vp), ("w", vp), ("c", vp),
                 ("bias", vp), ("gate", vp), ("qkv", C.POINTER(QkvEpi)), ("euler", C.POINTER(EulerEpi)),
-                ("fork", vp)]
+                ("conv", C.POINTER(ConvTaps)), ("fork", vp)]
 
 
 class AttnArgs(C.Structure):
@@ -90,6 +94,10 @@ _SIGS = {
     "lp_silu": ([vp, vp, C.c_int, C.c_int, vp], C.c_int),
     "lp_patchify": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
     "lp_oracle_step": ([vp, vp, C.c_float, C.c_float, vp, vp, i64, vp], C.c_int),
+    "lp_vae_pack_latent": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp], C.c_int),
+    "lp_vae_norm_silu": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp], C.c_int),
+    "lp_vae_upsample": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp], C.c_int),
+    "lp_vae_frames": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp], C.c_int),
     "lp_unpatchify_euler": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp],
                             C.c_int),
     "lp_fork_create": ([C.POINTER(vp)], C.c_int),

@@ -20,7 +20,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "liblivepipe_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["lp_api.cu", "lp_f32.cu", "lp_rows.cu", "lp_links.cu", "lp_gemm_tc.cu", "lp_attn_tc.cu", "lp_codec.cu", "lp_vmm.cu"]
+SOURCES = ["lp_api.cu", "lp_f32.cu", "lp_rows.cu", "lp_links.cu", "lp_gemm_tc.cu", "lp_attn_tc.cu", "lp_codec.cu", "lp_vmm.cu", "lp_vae.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",

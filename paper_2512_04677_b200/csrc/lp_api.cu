@@ -57,6 +57,11 @@ int preload_rows();
 int preload_gemm_tc();
 int preload_attn_tc();
 int preload_codec();
+int preload_vae();
+int vae_pack_latent(const float*, int, int, int, int, int, void*, cudaStream_t);
+int vae_norm_silu(const float*, const float*, int, int, int, int, int, float, void*, cudaStream_t);
+int vae_upsample(const void*, int, int, int, int, int, void*, cudaStream_t);
+int vae_frames(const float*, int, int, int, int, int, float*, cudaStream_t);
 int fork_create(void**);
 int fork_destroy(void*);
 int codec_patch_decode(const float*, int, int, int, int, const float*, int, int, int, float*, cudaStream_t);
@@ -90,7 +95,7 @@ int lp_init(int device) {
   // loaded kernel launched while a waiter spins can stall in the loader.
   int rc;
   if ((rc = preload_links()) || (rc = preload_f32()) || (rc = preload_rows()) || (rc = preload_gemm_tc()) ||
-      (rc = preload_attn_tc()) || (rc = preload_codec()))
+      (rc = preload_attn_tc()) || (rc = preload_codec()) || (rc = preload_vae()))
     return rc;
   return tma_init();
 }
@@ -103,6 +108,7 @@ int lp_gemm(const lp_gemm_args* a, void* stream) {
   LP_CHECK_ARG(a->m >= 0 && a->n > 0 && a->k > 0, "lp_gemm: bad shape");
   if (a->in_dtype == LP_BF16) return gemm_tc(a, S(stream));
   LP_CHECK_ARG(a->in_dtype == LP_F32, "lp_gemm: in_dtype must be LP_F32 or LP_BF16");
+  if (a->conv) return fail(LP_EUNSUPPORTED, "lp_gemm: conv taps need bf16 operands");
   if (a->epilogue == LP_EPI_QKV)
     return fail(LP_EUNSUPPORTED, "lp_gemm: fp32 QKV epilogue is lp_gemm(STORE) + lp_qkv_post");
   if (a->epilogue == LP_EPI_EULER)
@@ -288,3 +294,18 @@ int lp_ipc_open(const uint8_t* handle, int64_t offset, void** ptr_out) { return 
 int lp_ipc_close(void* mapped_base) { return ipc_close(mapped_base); }
 
 }  // extern "C"
+
+// ---- decode stage: VAE stand-in row kernels (lp_vae.cu) ----
+int lp_vae_pack_latent(const float* x, int f, int c, int h, int w, int cpad, void* out, void* stream) {
+  return vae_pack_latent(x, f, c, h, w, cpad, out, S(stream));
+}
+int lp_vae_norm_silu(const float* hbuf, const float* gamma, int t, int h, int w, int c, int mode, float eps,
+                     void* out, void* stream) {
+  return vae_norm_silu(hbuf, gamma, t, h, w, c, mode, eps, out, S(stream));
+}
+int lp_vae_upsample(const void* in, int t, int h, int w, int c, int ft, void* out, void* stream) {
+  return vae_upsample(in, t, h, w, c, ft, out, S(stream));
+}
+int lp_vae_frames(const float* hbuf, int t, int h, int w, int cpad, int cout, float* frames, void* stream) {
+  return vae_frames(hbuf, t, h, w, cpad, cout, frames, S(stream));
+}

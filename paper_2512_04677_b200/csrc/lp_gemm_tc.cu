@@ -37,7 +37,22 @@ struct GemmParams {
   const float* gate;
   lp_qkv_epi qkv;
   lp_euler_epi euler;
+  // implicit-GEMM conv (lp_conv_taps): k-chunk kb reads A rows m0 + tap_row[kb / conv_kpt],
+  // columns (kb % conv_kpt) * GBK; conv_kpt = 0 for a plain GEMM
+  int conv_kpt;
+  int tap_row[27];
 };
+
+__device__ __forceinline__ void a_coords(const GemmParams& p, int kb, int m0, int& col, int& row) {
+  if (p.conv_kpt) {
+    const int t = kb / p.conv_kpt;
+    col = (kb - t * p.conv_kpt) * GBK;
+    row = m0 + p.tap_row[t];
+  } else {
+    col = kb * GBK;
+    row = m0;
+  }
+}
 
 struct ForkCtx {
   cudaStream_t side;
@@ -285,7 +300,9 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           uint8_t* sa = smem + stage * SM::STAGE_BYTES;
           uint8_t* sb = sa + SM::A_BYTES;
           mbar_arrive_expect_tx(&full[stage], SM::STAGE_BYTES);
-          tma_load_2d_hint(sa, &tmA, &full[stage], kb * GBK, m0, pol_a);
+          int ac, ar;
+          a_coords(p, kb, m0, ac, ar);
+          tma_load_2d_hint(sa, &tmA, &full[stage], ac, ar, pol_a);
           tma_load_2d(sb, &tmB, &full[stage], kb * GBK, n0);
           if (++stage == GSTAGES) {
             stage = 0;
@@ -526,7 +543,8 @@ static int launch_gemm_tc2(const lp_gemm_args* a, const GemmParams& p, cudaStrea
 template <int BN>
 static int launch_gemm_tc(const lp_gemm_args* a, const GemmParams& p, cudaStream_t st) {
   CUtensorMap ta, tb;
-  int rc = make_tmap_bf16_2d(&ta, a->a, (uint64_t)a->m, (uint64_t)a->k, (uint64_t)a->lda, GBM, GBK);
+  const uint64_t a_cols = p.conv_kpt ? (uint64_t)p.conv_kpt * GBK : (uint64_t)a->k;  // conv: A is [rows, cin]
+  int rc = make_tmap_bf16_2d(&ta, a->a, (uint64_t)a->m, a_cols, (uint64_t)a->lda, GBM, GBK);
   if (rc) return rc;
   rc = make_tmap_bf16_2d(&tb, a->w, (uint64_t)a->n, (uint64_t)a->k, (uint64_t)a->ldw, BN, GBK);
   if (rc) return rc;
@@ -633,6 +651,21 @@ int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
   p.gate = a->gate;
   memset(&p.qkv, 0, sizeof(p.qkv));
   memset(&p.euler, 0, sizeof(p.euler));
+  p.conv_kpt = 0;
+  if (a->conv) {
+    const lp_conv_taps& cv = *a->conv;
+    LP_CHECK_ARG(cv.n_taps >= 1 && cv.n_taps <= 27 && cv.cin % GBK == 0 && a->k == cv.n_taps * cv.cin,
+                 "gemm_tc: conv needs 1..27 taps, cin % 64 == 0 and k == n_taps * cin");
+    LP_CHECK_ARG(a->epilogue == LP_EPI_STORE || a->epilogue == LP_EPI_RESID, "gemm_tc: conv epilogue STORE/RESID");
+    LP_CHECK_ARG(a->lda == cv.cin, "gemm_tc: conv A is [rows, cin] (lda == cin)");
+    p.conv_kpt = cv.cin / GBK;
+    for (int t = 0; t < cv.n_taps; ++t) p.tap_row[t] = cv.tap_row[t];
+    // single-CTA tiles: the A box of a tap is one row-shifted 128-row window
+    if (a->n % 256 == 0) return launch_gemm_tc<256>(a, p, st);
+    if (a->n % 128 == 0) return launch_gemm_tc<128>(a, p, st);
+    if (a->n % 64 == 0) return launch_gemm_tc<64>(a, p, st);
+    return fail(LP_EUNSUPPORTED, "gemm_tc: conv n must be a multiple of 64");
+  }
   if (a->epilogue == LP_EPI_EULER) {
     LP_CHECK_ARG(a->euler != nullptr && a->euler->x_in && a->euler->x_out && a->euler->desc,
                  "gemm_tc: EULER epilogue needs euler args");
