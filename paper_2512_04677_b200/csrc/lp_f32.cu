@@ -131,26 +131,58 @@ __global__ void qkv_post_kernel(const float* __restrict__ qkv, int m, lp_qkv_epi
 // ------------------------------------------------------------ attention ---
 // NumPy pairwise sum of a contiguous fp32 run (8 accumulators below 128
 // elements, recursive halving above) -- the order np.sum(..., axis=-1) uses.
-__device__ float pairwise_sum(const float* a, int n) {
+// The halving recursion runs on an explicit stack: device recursion over
+// 24,960 logits overflowed the 1 KB per-thread call stack (compute-sanitizer
+// "Stack overflow", an illegal-address fault at the benched N_kv in fp32 mode).
+__device__ __forceinline__ float pairwise_leaf(const float* a, int n) {
   if (n < 8) {
     float r = 0.0f;  // NumPy starts from -0.0 only for empty input; 0.0 + x == x for x != -0
     for (int i = 0; i < n; ++i) r = __fadd_rn(r, a[i]);
     return r;
   }
-  if (n <= 128) {
-    float r[8];
-    for (int j = 0; j < 8; ++j) r[j] = a[j];
-    int i = 8;
-    for (; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], a[i + j]);
-    float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
-                          __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __fadd_rn(res, a[i]);
-    return res;
+  float r[8];
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], a[i + j]);
+  float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                        __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __fadd_rn(res, a[i]);
+  return res;
+}
+
+__device__ float pairwise_sum(const float* a, int n) {
+  // frames of the halving recursion: (offset, length, state: 0 new, 1 left
+  // pending, 2 right pending, left partial)
+  int off[26], len[26], state[26];
+  float left[26];
+  int sp = 0;
+  off[0] = 0, len[0] = n, state[0] = 0;
+  for (;;) {
+    if (len[sp] <= 128) {
+      float v = pairwise_leaf(a + off[sp], len[sp]);
+      for (;;) {  // deliver v to the parents
+        if (sp == 0) return v;
+        --sp;
+        if (state[sp] == 1) {  // left half done: descend into the right half
+          left[sp] = v;
+          state[sp] = 2;
+          int n2 = len[sp] / 2;
+          n2 -= n2 % 8;
+          off[sp + 1] = off[sp] + n2, len[sp + 1] = len[sp] - n2, state[sp + 1] = 0;
+          ++sp;
+          break;
+        }
+        v = __fadd_rn(left[sp], v);  // both halves done
+      }
+      continue;
+    }
+    int n2 = len[sp] / 2;
+    n2 -= n2 % 8;
+    state[sp] = 1;
+    off[sp + 1] = off[sp], len[sp + 1] = n2, state[sp + 1] = 0;
+    ++sp;
   }
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  return __fadd_rn(pairwise_sum(a, n2), pairwise_sum(a + n2, n - n2));
 }
 
 // One warp per (query row, head); logits row staged in shared memory.
