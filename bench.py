@@ -67,6 +67,16 @@ def profile_for(name):
     return WAN_14B if name == "14b" else WAN_1_3B
 
 
+def workload_config(args):
+    """The workload definition every arm of this bench reports as ``config``
+    (ours at any N and the reference arm): identical dicts for one command."""
+    prof = profile_for(args.config)
+    n_tok = 3 * prof.tokens_per_frame
+    return {"workload": workload(args.config), "steps_T": 4, "cache_L": 4, "tokens_per_block": n_tok,
+            "n_kv_steady": prof.tokens_per_frame + 4 * n_tok + n_tok, "history_sigma": args.history_sigma,
+            "l2": "inputs (weights + KV rings) >> 126 MB L2; no flush needed"}
+
+
 def workload(name):
     return {"14b": "Wan-14B-shape causal DiT (40 layers, dim 5120, 40 heads, ffn 13824), 4-step, 480p block",
             "1.3b": "Wan-1.3B-shape causal DiT (30 layers, dim 1536, 12 heads, ffn 8960), 4-step, 480p block"}[name]
@@ -139,29 +149,36 @@ def cpu_baseline(prof, n_tok, n_kv, steps, target_s=10.0):
 def run_reference(args):
     """--impl reference: the reference's CPU path (oracle port of its pinned
     matmul; the reference is Python and cannot travel to the GPU box) on all
-    host cores, W warm-up + K timed samples of ~6 s each (capped so the run
-    stays within a few minutes); rank 0 only under torchrun."""
+    host cores.  A step is one bounded sample of the workload (~6 s of
+    pinned-order matmul at the benchmark's token count, fewer seconds when K
+    is large so the run stays within a few minutes); ``value`` extrapolates
+    the measured rate to whole 14B blocks.  W warm-up samples of ~0.5 s.
+    Rank 0 only under torchrun."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     prof = profile_for(args.config)
     n_tok = 3 * prof.tokens_per_frame
     n_kv = prof.tokens_per_frame + 5 * n_tok
-    k = max(1, min(args.steps, 20))
-    w = min(args.warmup, 1)
-    per = min(6.0, 150.0 / (k + w))
+    k, w = max(1, args.steps), max(0, args.warmup)
+    per = min(6.0, 150.0 / k)
     for _ in range(w):
-        cpu_baseline(prof, n_tok, n_kv, 4, target_s=per)
-    vals, cb = [], None
+        cpu_baseline(prof, n_tok, n_kv, 4, target_s=0.5)
+    vals, walls, cb = [], [], None
     for _ in range(k):
+        t0 = time.perf_counter()
         cb = cpu_baseline(prof, n_tok, n_kv, 4, target_s=per)
+        walls.append(time.perf_counter() - t0)
         vals.append(cb["value"])
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "FPS", "n_gpus": args.gpus,
-            "steps": k, "warmup": w, "ms_per_step": 1e3 * FRAMES_PER_BLOCK_VIDEO / v,
+            "steps": k, "warmup": w, "ms_per_step": 1e3 * statistics.mean(walls),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": workload(args.config), "executor": "reference CPU "
-                                            "algorithm (oracle port of numerics.matmul), all host cores"},
+            "data": "synthetic", "config": workload_config(args),
+            "execution": {"executor": "reference CPU algorithm (oracle port of numerics.matmul), all host cores",
+                          "step": "one bounded sample (pinned-order matmul at the block's token count); value = "
+                                  "the sampled rate extrapolated linearly in FLOPs to whole blocks",
+                          "sec_per_block_extrapolated": FRAMES_PER_BLOCK_VIDEO / v},
             "cpu_baseline": {"value": v, "unit": "FPS", "cores": cb["cores"], "kind": "port",
                              "sample": cb["sample"]},
             "e2e": {"value": v, "unit": "FPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -240,7 +257,7 @@ def roofline(prof, kern, n_tok, n_kv):
     if "attention" not in kern:
         return None
     ach = kern["attention"]["tflops"]
-    return {"bound": "tensor", "kernel": "attn_tc_kernel (tcgen05 flash attention, one layer, all heads)",
+    return {"bound": "tensor", "kernel": "attn_tc2_kernel (cluster-pair tcgen05 flash attention + exact-rerun check + tail combine, one layer, all heads)",
             "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach / peak_tf, "traffic": TRAFFIC.get(
                 "attention"), "flops_per_launch": flops["attention"], "avg_launch_ms": kern["attention"]["avg_ms"],
             "share_of_step": kern["attention"]["share"], "frac_of_burst_peak": ach / burst_tf,
@@ -388,10 +405,8 @@ def run_ours(args):
         "metric": METRIC, "value": fps, "unit": "FPS", "n_gpus": 1, "steps": K, "warmup": W,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (device-RNG random-init weights, N(0,1) noise blocks)",
-        "config": {"workload": workload(args.config), "steps_T": T, "cache_L": Lc, "tokens_per_block": n_tok,
-                   "n_kv_steady": n_kv_steady, "parallelism": "1 GPU, T steps sequential (TPP stages collapsed)",
-                   "history_sigma": args.history_sigma,
-                   "l2": "inputs (weights + KV rings) >> 126 MB L2; no flush needed",
+        "config": workload_config(args),
+        "execution": {"parallelism": "1 GPU, T steps sequential (TPP stages collapsed)",
                    "block_latency_ms": ms_step, "achieved_tflops": ach, "frac_of_sustained_peak": ach / peak_tf,
                    "frac_of_burst_peak": ach / burst_tf,
                    "roofline_fps_sustained": FRAMES_PER_BLOCK_VIDEO / (flops_block / (peak_tf * 1e12)),
@@ -437,7 +452,7 @@ def run_dist(args, rank, world, local):
     T, Lc = 4, 4
     cfg = lp.EngineConfig(mode="tpp", steps=T, cache_capacity=Lc, frames_per_block=3, profile=prof,
                           precision="bf16", devices=(local,), device_inputs=True, blocks=1 << 20,
-                          link_capacity=2, link_timeout_s=600.0)
+                          link_capacity=2, link_timeout_s=600.0, vae_decode=args.decode_gpu)
     run = tpp_dist.DistTPP(cfg, transport="ipc", device=local, decode_gpu=args.decode_gpu)
     role = run.role
     be = run.backend
@@ -523,13 +538,12 @@ def run_dist(args, rank, world, local):
             "metric": METRIC, "value": fps, "unit": "FPS", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": 1e3 * job_s / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (device-RNG random-init weights, N(0,1) noise blocks)",
-            "config": {"workload": workload(args.config), "steps_T": T, "cache_L": Lc, "tokens_per_block": n_tok,
-                       "n_kv_steady": n_kv_steady,
+            "config": workload_config(args),
+            "execution": {
                        "parallelism": f"TPP: {role.n_pipes} pipeline(s) x {len(role.ranks)} GPUs "
                                       f"(steps per GPU {[r.steps for r in run.roles[:len(role.ranks)]]}"
                                       f"{', last = decode rank' if args.decode_gpu else ''}), "
                                       "latents over NVLink P2P (CUDA IPC links, fused epilogue stores)",
-                       "l2": "inputs (weights + KV rings) >> 126 MB L2; no flush needed",
                        "steady_fps_last_stage": float(steady_t.item()) * role.n_pipes,
                        "timed_region": "K pipeline steps (every stage one block) after a staggered "
                                        "warm-up that fills the pipeline; barrier-bracketed, max over ranks",

@@ -394,6 +394,21 @@ __global__ void history_noise_kernel(T* __restrict__ arena, int d, const float* 
 // radius uniform: tail cut at 5.4 sigma, P = 7e-8; 12-bit angle) -- with one
 // 16-byte load and store and 32-bit index math.  Half the RNG and index work
 // per element of history_noise_kernel; the parity path (host draws) is above.
+// cos / sin of the 4096 Box-Muller angles ((a + 0.5) * 2 pi / 4096): built
+// once per device at lp_init with the same __sincosf, so the table lookup
+// gives bit-identical noise and takes two of every four MUFU ops per pair
+// off the RNG-bound kernel.
+__device__ float2 g_bm_angle[4096];
+
+__global__ void bm_table_kernel() {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 4096) {
+    float sn, cs;
+    __sincosf(((float)i + 0.5f) * 1.5339807878856412e-03f, &sn, &cs);
+    g_bm_angle[i] = make_float2(cs, sn);
+  }
+}
+
 __device__ __forceinline__ void normal8_fast(uint64_t seed, uint64_t stream, uint32_t ctr, float* z) {
   const uint4 c = make_uint4(ctr, 0x9E3779B9u, (uint32_t)stream, (uint32_t)(stream >> 32));
   const uint2 k = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
@@ -402,12 +417,10 @@ __device__ __forceinline__ void normal8_fast(uint64_t seed, uint64_t stream, uin
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const float u = ((float)(w[j] >> 12) + 0.5f) * 9.5367431640625e-07f;  // 2^-20
-    const float a = ((float)(w[j] & 0xFFFu) + 0.5f) * 1.5339807878856412e-03f;  // 2 pi / 4096
     const float rad = sqrtf(-2.0f * __logf(u));
-    float sn, cs;
-    __sincosf(a, &sn, &cs);
-    z[2 * j] = rad * cs;
-    z[2 * j + 1] = rad * sn;
+    const float2 cs = __ldg(&g_bm_angle[w[j] & 0xFFFu]);  // angle (a + 0.5) * 2 pi / 4096
+    z[2 * j] = rad * cs.x;
+    z[2 * j + 1] = rad * cs.y;
   }
 }
 
@@ -446,6 +459,19 @@ static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 int preload_rows() {
   cudaFuncAttributes a;
+  {  // the Box-Muller angle table, once per device (lp_init may be called again later)
+    static bool built[64] = {};
+    int dev = 0;
+    LP_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 64 && !built[dev]) {
+      cudaStream_t s;
+      LP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      bm_table_kernel<<<16, 256, 0, s>>>();
+      LP_CUDA_TRY(cudaStreamSynchronize(s));
+      LP_CUDA_TRY(cudaStreamDestroy(s));
+      built[dev] = true;
+    }
+  }
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, cond_row_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, add_row_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_kernel<float, 256>));

@@ -97,6 +97,10 @@ class EngineConfig:
     patch_codec: bool = False
     pixel_channels: int = 3
     pixel_scale: int = 8
+    # the dedicated decode rank (tpp_dist, decode_gpu) also runs the VAE
+    # stand-in (vae.VaeDecoder) on every received block -- the decode GPU's
+    # realistic cost; frames stay in its HBM
+    vae_decode: bool = False
 
     def __post_init__(self):
         if self.mode not in MODES:

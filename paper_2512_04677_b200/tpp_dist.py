@@ -278,6 +278,20 @@ class DecodeBackend:
         self.status = _status_word()
         self.stages = []
         self.fused = None
+        self.vae = self.frames = None
+        if cfg.vae_decode and prof.patched:  # buffers allocated now, not while a link kernel spins
+            from .vae import VaeDecoder
+
+            self.vae = VaeDecoder(prof.channels, prof.height, prof.width, f"cuda:{device}")
+            self.frames = torch.empty((4 * cfg.frames_per_block, 3 * 64 * prof.height * prof.width),
+                                      device=f"cuda:{device}")
+            with torch.cuda.stream(self.stream):
+                self.vae.decode_into(self.buf, self.frames, self.stream)
+            self.stream.synchronize()
+
+    def _vae_decode(self) -> None:
+        if self.vae is not None:
+            self.vae.decode_into(self.buf, self.frames, self.stream)
 
     def capture(self) -> None:
         pass
@@ -293,6 +307,7 @@ class DecodeBackend:
 
     def read_output(self, out: torch.Tensor | None = None) -> np.ndarray | None:
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            self._vae_decode()
             if out is not None:
                 out.copy_(self.buf.reshape(out.shape), non_blocking=True)
                 return None

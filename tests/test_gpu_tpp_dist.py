@@ -80,6 +80,20 @@ def test_ipc_tpp_decode_rank_runs_patch_codec(tmp_path):
     assert rec["frames_sha256"] == hashlib.sha256(seq.frames.astype("<f4").tobytes()).hexdigest()
 
 
+def test_ipc_4_plus_1_layout_with_vae_decode_rank(tmp_path):
+    # the paper's 4 DiT + 1 VAE GPU layout (4 stage ranks + the decode rank
+    # running the VAE stand-in on every received block), 5 ranks sharing one
+    # GPU: the latents equal the single-process sequential run bitwise
+    kw = dict(steps=4, blocks=3, cache_capacity=2, vae_decode=1)
+    out = tmp_path / "res"
+    launch(5, "gpu", out, dict(kw, precision="bf16", profile="wan_small", link_timeout_s=90.0, decode_gpu=1),
+           timeout=900)
+    got = np.load(f"{out}.0.npy")
+    seq = lp.run_sequential(lp.EngineConfig(mode="sequential", precision="bf16", profile=wan_small(),
+                                            **dict(kw, vae_decode=False)))
+    assert got.tobytes() == np.stack([b.values for b in seq.blocks]).tobytes()
+
+
 def test_ipc_two_pipelines_of_four_ranks(tmp_path):
     # the 8-GPU layout (two independent 4-stage pipelines, different noise
     # seeds) with 8 ranks sharing one GPU: each pipeline equals the
