@@ -185,18 +185,22 @@ __device__ float pairwise_sum(const float* a, int n) {
   }
 }
 
-// One warp per (query row, head); logits row staged in shared memory.
+// One 128-thread CTA per (query row, head); the logits row in shared memory.
+// Every value is produced in the reference's order (bit-identical to the
+// round-1 one-warp-per-row kernel, 4x its parallelism): logit j = ascending-c
+// fp32 dot product * scale (thread j % 128), row max, exp, NumPy pairwise row
+// sum (thread 0), normalise, then out[c] = ascending-key chain (thread c).
 template <typename T>
-__global__ void attn_f32_kernel(const T* __restrict__ q, const T* __restrict__ karena,
-                                const T* __restrict__ varena, T* __restrict__ out, int n_q,
-                                int n_heads, int hd, float scale, const lp_block_desc* __restrict__ desc,
-                                int n_kv_max) {
-  extern __shared__ float smem[];
-  const int wib = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int warp = blockIdx.x * (blockDim.x / 32) + wib;
-  const int row = warp / n_heads, head = warp % n_heads;
+__global__ void __launch_bounds__(128) attn_f32_kernel(const T* __restrict__ q, const T* __restrict__ karena,
+                                                       const T* __restrict__ varena, T* __restrict__ out, int n_q,
+                                                       int n_heads, int hd, float scale,
+                                                       const lp_block_desc* __restrict__ desc, int n_kv_max) {
+  extern __shared__ float logit[];
+  __shared__ float red[4];
+  __shared__ float total_sum;
+  const int tid = threadIdx.x, lane = tid % 32, wid = tid / 32;
+  const int row = blockIdx.x / n_heads, head = blockIdx.x % n_heads;
   if (row >= n_q) return;
-  float* logit = smem + (size_t)wib * n_kv_max;
   const int d = n_heads * hd;
   const T* qr = q + (int64_t)row * d + head * hd;
   // logits in reference key order: segments as listed in the descriptor
@@ -206,7 +210,7 @@ __global__ void attn_f32_kernel(const T* __restrict__ q, const T* __restrict__ k
   int base = 0;
   for (int s = 0; s < desc->n_seg; ++s) {
     const int r0 = desc->seg_row[s], len = desc->seg_len[s];
-    for (int j = lane; j < len; j += 32) {
+    for (int j = tid; j < len; j += blockDim.x) {
       const T* kr = karena + (int64_t)(r0 + j) * d + head * hd;
       float acc = 0.0f;
       for (int c = 0; c < hd; ++c) acc = __fadd_rn(acc, __fmul_rn(to_f32(qr[c]), to_f32(kr[c])));
@@ -215,26 +219,29 @@ __global__ void attn_f32_kernel(const T* __restrict__ q, const T* __restrict__ k
     base += len;
   }
   const int n_kv = base;
-  __syncwarp();
+  __syncthreads();
   float mx = -INFINITY;
-  for (int j = lane; j < n_kv; j += 32) mx = fmaxf(mx, logit[j]);
+  for (int j = tid; j < n_kv; j += blockDim.x) mx = fmaxf(mx, logit[j]);
 #pragma unroll
   for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  for (int j = lane; j < n_kv; j += 32) logit[j] = expf(__fsub_rn(logit[j], mx));
-  __syncwarp();
-  float sum = 0.0f;
-  if (lane == 0) sum = pairwise_sum(logit, n_kv);
-  sum = __shfl_sync(0xffffffffu, sum, 0);
-  for (int j = lane; j < n_kv; j += 32) logit[j] = __fdiv_rn(logit[j], sum);
-  __syncwarp();
-  // out = P . V, ascending key order (pinned), lanes over head columns
-  for (int c = lane; c < hd; c += 32) {
+  if (lane == 0) red[wid] = mx;
+  __syncthreads();
+  mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  for (int j = tid; j < n_kv; j += blockDim.x) logit[j] = expf(__fsub_rn(logit[j], mx));
+  __syncthreads();
+  if (tid == 0) total_sum = pairwise_sum(logit, n_kv);
+  __syncthreads();
+  const float sum = total_sum;
+  for (int j = tid; j < n_kv; j += blockDim.x) logit[j] = __fdiv_rn(logit[j], sum);
+  __syncthreads();
+  // out = P . V, ascending key order (pinned), one thread per head column
+  for (int c = tid; c < hd; c += blockDim.x) {
     float acc = 0.0f;
     int kb = 0;
     for (int s = 0; s < desc->n_seg; ++s) {
       const int r0 = desc->seg_row[s], len = desc->seg_len[s];
-      for (int j = 0; j < len; ++j)
-        acc = __fadd_rn(acc, __fmul_rn(logit[kb + j], to_f32(varena[(int64_t)(r0 + j) * d + head * hd + c])));
+      const T* vc = varena + (int64_t)r0 * d + head * hd + c;
+      for (int j = 0; j < len; ++j) acc = __fadd_rn(acc, __fmul_rn(logit[kb + j], to_f32(vc[(int64_t)j * d])));
       kb += len;
     }
     out[(int64_t)row * d + head * hd + c] = from_f32<T>(acc);
@@ -306,24 +313,22 @@ int qkv_post(const float* qkv, int m, const lp_qkv_epi& e, int out_dtype, cudaSt
 
 int attention_simt(const lp_attn_args* a, int n_kv_max, cudaStream_t st) {
   LP_CHECK_ARG(n_kv_max > 0, "attention: empty key set");
-  const size_t per_warp = (size_t)n_kv_max * sizeof(float);
-  int warps_per_block = (int)std::max<size_t>(1, std::min<size_t>(4, (160 * 1024) / per_warp));
-  LP_CHECK_ARG(per_warp <= 200 * 1024, "attention_simt: too many keys for validation mode");
-  const int warps = a->n_q * a->n_heads;
-  const int blocks = (warps + warps_per_block - 1) / warps_per_block;
-  const size_t smem = per_warp * warps_per_block;
+  const size_t smem = (size_t)n_kv_max * sizeof(float);
+  LP_CHECK_ARG(smem <= 200 * 1024, "attention_simt: too many keys for validation mode");
+  const int64_t blocks = (int64_t)a->n_q * a->n_heads;
+  if (blocks == 0) return LP_OK;
   if (a->dtype == LP_BF16) {
     auto k = attn_f32_kernel<__nv_bfloat16>;
     LP_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<blocks, warps_per_block * 32, smem, st>>>(
+    k<<<(unsigned)blocks, 128, smem, st>>>(
         (const __nv_bfloat16*)a->q, (const __nv_bfloat16*)a->k_arena, (const __nv_bfloat16*)a->v_arena,
         (__nv_bfloat16*)a->out, a->n_q, a->n_heads, a->head_dim, a->scale, a->desc, n_kv_max);
   } else {
     auto k = attn_f32_kernel<float>;
     LP_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<blocks, warps_per_block * 32, smem, st>>>((const float*)a->q, (const float*)a->k_arena,
-                                                 (const float*)a->v_arena, (float*)a->out, a->n_q,
-                                                 a->n_heads, a->head_dim, a->scale, a->desc, n_kv_max);
+    k<<<(unsigned)blocks, 128, smem, st>>>((const float*)a->q, (const float*)a->k_arena, (const float*)a->v_arena,
+                                           (float*)a->out, a->n_q, a->n_heads, a->head_dim, a->scale, a->desc,
+                                           n_kv_max);
   }
   return launch_status("attention_simt");
 }

@@ -129,3 +129,32 @@ def test_dataclasses_replace_yields_host_entry():
     h = dataclasses.replace(e, keys=keys)
     assert not h.on_device and h.block_index == 0 and h.timestep_index == 3
     assert np.array_equal(h.keys[0], e.keys[0] + 1.0) and np.array_equal(h.values[1], e.values[1])
+
+
+def test_dropin_14b_shape_fits_in_hbm():
+    # the drop-in at the 14B shape (40 layers, d 5120, 4,680 tokens per block):
+    # the reference engine's window of L=4 device entries plus the in-flight
+    # one through denoise_block; the VMM slot pool maps only what is alive,
+    # so device memory stays far below the 180 GB of HBM (the round-1 pool
+    # reserved ~385 GB up front)
+    import torch
+
+    from paper_2512_04677_b200.model import DeviceWeights
+
+    prof = lp.WAN_14B
+    dw = DeviceWeights.random(prof, "bf16", "cuda:0", 7)
+    sched = lp.TimestepSchedule.uniform(4)
+    dn = lp.B200Denoiser(None, sched, precision="bf16", device_weights=dw)
+    conds = lp.synthetic_conditions(11, 6, prof.audio_dim, prof.prompt_dim, prof.latent_dim)
+    cache = lp.RollingKvCache(4, 4)
+    rng = np.random.default_rng(0)
+    for i in range(6):
+        x = lp.LatentBlock(rng.standard_normal((3, prof.latent_dim), dtype=np.float32), i)
+        out = dn.denoise_block(x, 4, cache.view(), lp.BlockCond(conds.audio_for(i), conds.prompt),
+                               conds.reference, i + 1, max_entries=4)
+        assert np.isfinite(out.velocity).all()
+        cache.push(out.kv)
+    torch.cuda.empty_cache()  # allocator cache of earlier tests in this process
+    free, total = torch.cuda.mem_get_info(0)
+    used_gb = (total - free) / 1e9
+    assert used_gb < 120.0, used_gb
