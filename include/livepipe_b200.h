@@ -202,7 +202,15 @@ LP_API int lp_graph_kernel_count(void* graph, int64_t* count);
  * _attend_head (:152-158): softmax(q K^T / sqrt(hd)) V over the visible keys
  * [sink | history oldest->newest | current] (segments from desc), no mask.
  *   LP_F32 : SIMT, reference summation order (numpy pairwise row sum).
- *   LP_BF16: tcgen05 flash attention, S/O in TMEM, fp32 online softmax.
+ *   LP_BF16: tcgen05 flash attention on cluster pairs (cta_group::2, M = 256
+ *            per pair, half of every K/V tile per SM), S/P/O in TMEM.  With a
+ *            workspace: bounded-exponent softmax (each row's offset is the
+ *            exact max of its first KV tile; the result equals exact softmax
+ *            while later scores stay within 2^64 of it) and a rerun of any
+ *            work unit that left that window by the exact online-max kernel,
+ *            which also runs every unit when the workspace is NULL.
+ *            Environment A/B: LP_ATTN_EXACT=1 (exact kernel only),
+ *            LP_ATTN_SINGLE=1 (single-CTA bounded-exponent kernel).
  */
 typedef struct lp_attn_args {
   int32_t dtype;
@@ -216,12 +224,13 @@ typedef struct lp_attn_args {
   int32_t arena_rows;     /* rows in the arena (bounds for TMA)             */
   int32_t n_kv_max;       /* host-known upper bound of visible keys         */
   void* workspace;        /* LP_BF16: partials of KV-split work units (the
-                             tail of the grid is split to fill the last wave;
-                             NULL or too small => no splitting)             */
+                             tail of the grid is split to fill the last wave)
+                             and one window flag per CTA; NULL or too small
+                             => no splitting and the exact kernel           */
   int64_t workspace_bytes;
 } lp_attn_args;
 /* Bytes of lp_attn_args.workspace the tcgen05 attention uses for n_q queries
-   and n_heads heads on this device (0 when no unit is split).               */
+   and n_heads heads on this device (split partials + window flags).          */
 LP_API int lp_attention_workspace(int n_q, int n_heads, int head_dim, int64_t* bytes_out);
 LP_API int lp_attention(const lp_attn_args* args, void* stream);
 /* SIMT reference attention for either dtype (validation tool: same math,

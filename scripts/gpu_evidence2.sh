@@ -17,3 +17,10 @@ import torch, paper_2512_04677_b200 as lp
 d = lp.VaeDecoder(16, 60, 104, 'cuda:0'); x = torch.randn(3, 16*60*104, device='cuda'); f = torch.empty(12, 3*480*832, device='cuda')
 d.decode_into(x, f); torch.cuda.synchronize()" > $OUT/ncu_vae.log 2>&1
 ls -la $OUT
+# GEMM dispatch A/B (O-proj / FFN-down): pair + tail split (default), no split, pairs everywhere
+for ab in "" "LP_NO_PAIR_SPLIT=1" "LP_GEMM2_ALL=1"; do
+  env $ab timeout 420 python bench.py --no-cpu-baseline --steps 3 > $OUT/bench_ab_${ab:-default}.json 2> $OUT/bench_ab_${ab:-default}.err
+  python -c "import json; d=json.loads(open('$OUT/bench_ab_${ab:-default}.json').read().strip().splitlines()[-1]); print('${ab:-default}', round(d['value'],3), d['clocks']['sm_mhz'], {k: round(x['avg_ms'],4) for k,x in d['kernels'].items()})" >> $OUT/gemm_ab.txt 2>&1
+done
+timeout 420 python bench.py --history-sigma 0.1 --no-cpu-baseline > $OUT/bench_sigma.json 2> $OUT/bench_sigma.err
+cat $OUT/gemm_ab.txt
