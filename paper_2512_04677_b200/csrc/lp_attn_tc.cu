@@ -89,6 +89,7 @@ struct AttnParams {
   int* flags;     // bounded-exponent kernels: 1 = a row left the exponent window,
                   // rerun exactly; exact kernel: non-null = rerun only those
   int flag_pairs; // flags written per CTA of a cluster pair (2 per work unit)
+  int unit_base;  // first unit of this launch (the ragged tail runs as its own launch)
 };
 
 // Unit u -> (head, pair): regular units (both Q tiles valid) first, head-major
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     piece = v % p.split;
   }
   int head, pair;
-  unit_coords(p, unit, head, pair);
+  unit_coords(p, p.unit_base + unit, head, pair);
   const int q0 = pair * (2 * AT_M);
   const bool two = q0 + AT_M < p.n_q;  // tile B holds valid rows
 
@@ -748,7 +749,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
     piece = v % p.split;
   }
   int head, pair;
-  unit_coords(p, unit, head, pair);
+  unit_coords(p, p.unit_base + unit, head, pair);
   const int q0 = pair * (2 * AT_M) + (int)rank * AT_M;  // this CTA's first query row
 
   if (threadIdx.x == 0) {
@@ -1031,7 +1032,7 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnParams p) {
   const int n_units = p.pairs * p.n_heads;
   if (p.n_whole + k >= n_units) return;
   int head, pair;
-  unit_coords(p, p.n_whole + k, head, pair);
+  unit_coords(p, p.unit_base + p.n_whole + k, head, pair);
   const int row = pair * (2 * AT_M) + r;
   if (row >= p.n_q) return;
   const float2* ml = reinterpret_cast<const float2*>(p.part_ml);
@@ -1142,10 +1143,31 @@ static int64_t flag_bytes(int grid) { return ((int64_t)grid * 4 + 255) / 256 * 2
 
 static AttnPlan plan_pair(int n_q, int n_heads) { return plan_attention(n_q, n_heads, num_sms() / 2, 1.0); }
 
+// The product path: the pair kernel over the units whose 256 rows are all
+// valid, then the ragged query tail of every head (one 128-row tile) on the
+// single-CTA kernel -- a pair would spend a whole M = 256 unit on it.
+struct PairLayout {
+  AttnPlan main;      // regular units only
+  int n_tail = 0;     // ragged units (one per head) or 0
+  int64_t flags_main = 0, flags_tail = 0, bytes = 0;  // workspace offsets / total
+};
+static PairLayout pair_layout(int n_q, int n_heads) {
+  PairLayout L;
+  const int pairs = (n_q + 2 * AT_M - 1) / (2 * AT_M);
+  const bool ragged = (pairs - 1) * 2 * AT_M + AT_M >= n_q;
+  const int reg = pairs - (ragged ? 1 : 0);
+  if (reg > 0) L.main = plan_pair(reg * 2 * AT_M, n_heads);
+  L.n_tail = ragged ? n_heads : 0;
+  L.flags_main = partial_bytes(L.main);
+  L.flags_tail = L.flags_main + flag_bytes(2 * L.main.grid());
+  L.bytes = L.flags_tail + flag_bytes(L.n_tail);
+  return L;
+}
+
 int64_t attention_workspace_bytes(int n_q, int n_heads) {
   if (n_q <= 0 || n_heads <= 0 || num_sms() <= 0) return 0;
-  const AttnPlan p1 = plan_attention(n_q, n_heads, num_sms()), p2 = plan_pair(n_q, n_heads);
-  return std::max(partial_bytes(p1), partial_bytes(p2)) + flag_bytes(2 * std::max(p1.grid(), p2.grid()));
+  const AttnPlan p1 = plan_attention(n_q, n_heads, num_sms());
+  return std::max(partial_bytes(p1) + flag_bytes(p1.grid()), pair_layout(n_q, n_heads).bytes);
 }
 
 int attention_tc(const lp_attn_args* a, cudaStream_t st) {
@@ -1162,17 +1184,7 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
   if (rc) return rc;
   // cluster-pair kernel (default) or the single-CTA one (LP_ATTN_SINGLE=1, A/B)
   const bool pair_k = getenv("LP_ATTN_SINGLE") == nullptr && getenv("LP_ATTN_EXACT") == nullptr;
-  AttnPlan pl = pair_k ? plan_pair(a->n_q, a->n_heads) : plan_attention(a->n_q, a->n_heads, num_sms());
   const int64_t have = a->workspace ? a->workspace_bytes : 0;
-  const int fl_words = (pair_k ? 2 : 1) * pl.grid();
-  if (pl.pieces() > 0 && have < partial_bytes(pl) + flag_bytes(fl_words)) {
-    pl.n_whole = pl.n_units;  // no (or too small a) workspace: run every unit whole
-    pl.split = 1;
-  }
-  // the bounded-exponent kernels need the flag words (after the partials);
-  // without them the exact single-CTA kernel runs every unit
-  const bool fast = have >= partial_bytes(pl) + flag_bytes((pair_k ? 2 : 1) * pl.grid()) &&
-                    getenv("LP_ATTN_EXACT") == nullptr;
   AttnParams p;
   p.n_q = a->n_q;
   p.n_heads = a->n_heads;
@@ -1180,25 +1192,73 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
   p.out = static_cast<__nv_bfloat16*>(a->out);
   p.ldo = d;
   p.desc = a->desc;
+  p.part_o = static_cast<float*>(a->workspace);
+  p.unit_base = 0;
+  const int smem = AttnSmem::TOTAL;
+  if (pair_k) {
+    const PairLayout lay = pair_layout(a->n_q, a->n_heads);
+    if (have >= lay.bytes) {
+      char* ws = static_cast<char*>(a->workspace);
+      const AttnPlan full = plan_attention(a->n_q, a->n_heads, num_sms());  // unit numbering (pairs, reg_pairs)
+      p.pairs = full.pairs;
+      p.reg_pairs = full.reg_pairs;
+      LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      if (lay.main.n_units > 0) {
+        const AttnPlan& pm = lay.main;
+        AttnParams q = p;
+        q.n_whole = pm.n_whole;
+        q.split = pm.split;
+        q.part_ml = q.part_o + pm.pieces() * (2 * AT_M) * AT_D;
+        q.flags = reinterpret_cast<int*>(ws + lay.flags_main);
+        q.flag_pairs = 1;
+        CUtensorMap tk2;  // this CTA's 64 keys of a tile
+        rc = make_tmap_bf16_2d(&tk2, a->k_arena, (uint64_t)a->arena_rows, (uint64_t)d, (uint64_t)d, 64, 64);
+        if (rc) return rc;
+        LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Attn2Smem::TOTAL));
+        attn_tc2_kernel<<<2 * pm.grid(), AT_THREADS, Attn2Smem::TOTAL, st>>>(tq, tk2, tv, q);
+        if ((rc = launch_status("attention_tc2"))) return rc;
+        attn_tc_kernel<false><<<pm.grid(), AT_THREADS, smem, st>>>(tq, tk, tv, q);  // rerun flagged units
+        if ((rc = launch_status("attention_tc"))) return rc;
+        if (pm.n_whole < pm.n_units) {
+          const int64_t warps = (int64_t)(pm.n_units - pm.n_whole) * (2 * AT_M);
+          attn_combine_kernel<<<(int)((warps * 32 + 255) / 256), 256, 0, st>>>(q);
+          if ((rc = launch_status("attention_combine"))) return rc;
+        }
+      }
+      if (lay.n_tail > 0) {  // ragged query tails: single-CTA kernel, tile B skipped
+        AttnParams q = p;
+        q.unit_base = full.reg_pairs * a->n_heads;
+        q.n_whole = lay.n_tail;
+        q.split = 1;
+        q.part_ml = nullptr;
+        q.flags = reinterpret_cast<int*>(ws + lay.flags_tail);
+        q.flag_pairs = 0;
+        LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attn_tc_kernel<true><<<lay.n_tail, AT_THREADS, smem, st>>>(tq, tk, tv, q);
+        if ((rc = launch_status("attention_tc_window"))) return rc;
+        attn_tc_kernel<false><<<lay.n_tail, AT_THREADS, smem, st>>>(tq, tk, tv, q);
+        if ((rc = launch_status("attention_tc"))) return rc;
+      }
+      return LP_OK;
+    }
+  }
+  AttnPlan pl = plan_attention(a->n_q, a->n_heads, num_sms());
+  if (pl.pieces() > 0 && have < partial_bytes(pl) + flag_bytes(pl.grid())) {
+    pl.n_whole = pl.n_units;  // no (or too small a) workspace: run every unit whole
+    pl.split = 1;
+  }
+  // the bounded-exponent kernel needs the flag words (after the partials);
+  // without them the exact single-CTA kernel runs every unit
+  const bool fast = have >= partial_bytes(pl) + flag_bytes(pl.grid()) && getenv("LP_ATTN_EXACT") == nullptr;
   p.pairs = pl.pairs;
   p.reg_pairs = pl.reg_pairs;
   p.n_whole = pl.n_whole;
   p.split = pl.split;
-  p.part_o = static_cast<float*>(a->workspace);
   p.part_ml = p.part_o ? p.part_o + pl.pieces() * (2 * AT_M) * AT_D : nullptr;
   p.flags = fast ? reinterpret_cast<int*>(static_cast<char*>(a->workspace) + partial_bytes(pl)) : nullptr;
-  p.flag_pairs = fast && pair_k;
-  const int smem = AttnSmem::TOTAL;
-  if (fast && pair_k) {
-    CUtensorMap tk2;  // this CTA's 64 keys of a tile
-    rc = make_tmap_bf16_2d(&tk2, a->k_arena, (uint64_t)a->arena_rows, (uint64_t)d, (uint64_t)d, 64, 64);
-    if (rc) return rc;
-    LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Attn2Smem::TOTAL));
-    attn_tc2_kernel<<<2 * pl.grid(), AT_THREADS, Attn2Smem::TOTAL, st>>>(tq, tk2, tv, p);
-    rc = launch_status("attention_tc2");
-    if (rc) return rc;
-  } else if (fast) {
+  p.flag_pairs = 0;
+  if (fast) {
     LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attn_tc_kernel<true><<<pl.grid(), AT_THREADS, smem, st>>>(tq, tk, tv, p);
     rc = launch_status("attention_tc_window");

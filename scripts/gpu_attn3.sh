@@ -1,0 +1,13 @@
+#!/bin/bash
+OUT=gpurun_out/${1:-a3}
+mkdir -p $OUT
+timeout 300 python -m pytest tests/test_gpu_attn.py -x -q --timeout 120 > $OUT/pytest_attn.log 2>&1
+echo "rc=$?" >> $OUT/pytest_attn.log
+if grep -q " passed" $OUT/pytest_attn.log && ! grep -q "failed\|Timeout\|rc=[1-9]" $OUT/pytest_attn.log; then
+  timeout 420 python bench.py --no-cpu-baseline > $OUT/bench.json 2> $OUT/bench.err
+  LP_ATTN_SINGLE=1 timeout 420 python bench.py --no-cpu-baseline --no-decode --steps 3 > $OUT/bench_single.json 2> $OUT/bench_single.err
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-probe --no-decode > $OUT/bench_ncu.log 2>&1
+fi
+tail -3 $OUT/pytest_attn.log
+for f in bench bench_single; do python -c "import json; d=json.loads(open('$OUT/$f.json').read().strip().splitlines()[-1]); print('$f', round(d['value'],3), d['clocks']['sm_mhz'], {k: round(x['avg_ms'],4) for k,x in d['kernels'].items()})"; done
