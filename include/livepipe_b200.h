@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LP_ABI_VERSION 5
+#define LP_ABI_VERSION 6
 
 /* status codes */
 #define LP_OK 0
@@ -228,6 +228,11 @@ typedef struct lp_attn_args {
                              and one window flag per CTA; NULL or too small
                              => no splitting and the exact kernel           */
   int64_t workspace_bytes;
+  void* fork;             /* lp_fork_create handle or NULL: the ragged query
+                             tails (one 128-row tile per head) run on the
+                             handle's side stream, concurrently with the
+                             cluster-pair grid (fork/join events on `stream`;
+                             graph-capture safe); NULL: after it            */
 } lp_attn_args;
 /* Bytes of lp_attn_args.workspace the tcgen05 attention uses for n_q queries
    and n_heads heads on this device (split partials + window flags).          */

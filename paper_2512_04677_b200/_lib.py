@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LIVEPIPE_LIB") or os.path.join(HERE, "liblivepipe_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "livepipe_b200.h")
 
-ABI_VERSION = 5  # LP_ABI_VERSION in include/livepipe_b200.h
+ABI_VERSION = 6  # LP_ABI_VERSION in include/livepipe_b200.h
 LP_OK, LP_EINVAL, LP_ECUDA, LP_EUNSUPPORTED, LP_ETIMEOUT, LP_EABORT = range(6)
 LP_F32, LP_BF16 = 0, 1
 EPI_STORE, EPI_RELU, EPI_GELU, EPI_RESID, EPI_QKV, EPI_EULER = range(6)
@@ -71,7 +71,8 @@ class GemmArgs(C.Structure):
 class AttnArgs(C.Structure):
     _fields_ = [("dtype", i32), ("n_q", i32), ("n_heads", i32), ("head_dim", i32), ("scale", f32),
                 ("q", vp), ("k_arena", vp), ("v_arena", vp), ("out", vp), ("desc", vp),
-                ("arena_rows", i32), ("n_kv_max", i32), ("workspace", vp), ("workspace_bytes", i64)]
+                ("arena_rows", i32), ("n_kv_max", i32), ("workspace", vp), ("workspace_bytes", i64),
+                ("fork", vp)]
 
 
 _SIGS = {

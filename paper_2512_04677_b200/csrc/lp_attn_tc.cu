@@ -692,12 +692,16 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 // other's TMEM-load and barrier latency; with the bounded-exponent offset
 // (max of tile 0, handed to warpgroup 1 once) they share one offset and never
 // synchronise per tile; their row sums are added at the end.
-//   warp 0      TMA producer (both CTAs): Q once, K/V halves (4-stage rings),
-//               completion counted on the leader's barriers
+//   warp 0      TMA producer (both CTAs): Q once, the K halves (4-stage ring)
+//   warp 3      TMA producer (both CTAs): the V halves (4-stage ring); both
+//               count completion on the leader's barriers
 //   warp 1      TMEM allocation (both); leader: issues the S = Q K^T MMAs
 //   warp 2      leader: issues the O += P V MMAs
 //   warps 4-7   softmax of tiles 0, 2, 4, ...    warps 8-11  tiles 1, 3, 5, ...
-constexpr int A2_KS = 4, A2_VS = 4;          // K / V ring stages
+#ifndef LP_ATTN2_KS
+#define LP_ATTN2_KS 4
+#endif
+constexpr int A2_KS = LP_ATTN2_KS, A2_VS = 4;  // K / V ring stages
 constexpr int A2_KT = 64 * AT_D * 2;         // 16 KB: this CTA's 64 keys x 128 dims
 constexpr int A2_KHALF = 64 * 64 * 2;        // 8 KB: one 64-dim SW128 block of it
 constexpr int A2_VT = AT_N * 64 * 2;         // 16 KB: 128 keys x this CTA's 64 dims
@@ -789,29 +793,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
   const int col0 = head * AT_D;
 
   if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(AT_REG_CTRL));
-  if (warp == 0) {
-    // ------------------------------------------------ TMA producer (both CTAs)
+  if (warp == 0 || warp == 3) {
+    // ------------------------------------------------ TMA producers (both CTAs):
+    // warp 0 loads Q and the K ring, warp 3 the V ring, so a K load never
+    // queues behind a V stage that PV has not released yet (S(t+2) needs
+    // K(t+2) early; V(t) is needed only after softmax(t))
     if (elect_one()) {
       const uint64_t pol = l2_policy_evict_last();
-      uint8_t* sq = smem + Attn2Smem::Q_OFF;
-      if (rank == 0) mbar_arrive_expect_tx(q_full, 2 * AT_TILE_BYTES);
-      tma_load_2d_2sm(sq, &tmQ, q_full, col0, q0, pol);
-      tma_load_2d_2sm(sq + AT_HALF, &tmQ, q_full, col0 + 64, q0, pol);
       TileCursor cur;
       cur.init(seg_row, seg_len, n_seg_s[0]);
       cur.skip(t_first);
-      for (int t = 0; t < n_tiles; ++t, cur.next()) {
-        const int ks = t % A2_KS, vs = t % A2_VS;
-        mbar_wait(&k_empty[ks], ((t / A2_KS) & 1) ^ 1);
-        if (rank == 0) mbar_arrive_expect_tx(&k_full[ks], 2 * A2_KT);
-        uint8_t* sk = smem + Attn2Smem::K_OFF + ks * A2_KT;
-        const int krow = cur.cur_row() + 64 * (int)rank;  // this CTA's 64 keys of the tile
-        tma_load_2d_2sm(sk, &tmK, &k_full[ks], col0, krow, pol);
-        tma_load_2d_2sm(sk + A2_KHALF, &tmK, &k_full[ks], col0 + 64, krow, pol);
-        mbar_wait(&v_empty[vs], ((t / A2_VS) & 1) ^ 1);
-        if (rank == 0) mbar_arrive_expect_tx(&v_full[vs], 2 * A2_VT);
-        tma_load_2d_2sm(smem + Attn2Smem::V_OFF + vs * A2_VT, &tmV, &v_full[vs], col0 + 64 * (int)rank,
-                        cur.cur_row(), pol);
+      if (warp == 0) {
+        uint8_t* sq = smem + Attn2Smem::Q_OFF;
+        if (rank == 0) mbar_arrive_expect_tx(q_full, 2 * AT_TILE_BYTES);
+        tma_load_2d_2sm(sq, &tmQ, q_full, col0, q0, pol);
+        tma_load_2d_2sm(sq + AT_HALF, &tmQ, q_full, col0 + 64, q0, pol);
+        for (int t = 0; t < n_tiles; ++t, cur.next()) {
+          const int ks = t % A2_KS;
+          mbar_wait(&k_empty[ks], ((t / A2_KS) & 1) ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&k_full[ks], 2 * A2_KT);
+          uint8_t* sk = smem + Attn2Smem::K_OFF + ks * A2_KT;
+          const int krow = cur.cur_row() + 64 * (int)rank;  // this CTA's 64 keys of the tile
+          tma_load_2d_2sm(sk, &tmK, &k_full[ks], col0, krow, pol);
+          tma_load_2d_2sm(sk + A2_KHALF, &tmK, &k_full[ks], col0 + 64, krow, pol);
+        }
+      } else {
+        for (int t = 0; t < n_tiles; ++t, cur.next()) {
+          const int vs = t % A2_VS;
+          mbar_wait(&v_empty[vs], ((t / A2_VS) & 1) ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&v_full[vs], 2 * A2_VT);
+          tma_load_2d_2sm(smem + Attn2Smem::V_OFF + vs * A2_VT, &tmV, &v_full[vs], col0 + 64 * (int)rank,
+                          cur.cur_row(), pol);
+        }
       }
     }
   } else if ((warp == 1 || warp == 2) && rank == 0) {
@@ -1203,6 +1216,16 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
       p.pairs = full.pairs;
       p.reg_pairs = full.reg_pairs;
       LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      // ragged query tails: single-CTA kernel (tile B skipped), on the fork's
+      // side stream when there is one -- forked before the pair grid is
+      // launched, so its CTAs take the SMs the pair grid's last wave leaves idle
+      const ForkCtx* fk = static_cast<const ForkCtx*>(a->fork);
+      cudaStream_t ts = st;
+      if (fk && lay.n_tail > 0 && lay.main.n_units > 0) {
+        LP_CUDA_TRY(cudaEventRecord(fk->fork, st));
+        LP_CUDA_TRY(cudaStreamWaitEvent(fk->side, fk->fork, 0));
+        ts = fk->side;
+      }
       if (lay.main.n_units > 0) {
         const AttnPlan& pm = lay.main;
         AttnParams q = p;
@@ -1226,7 +1249,7 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
           if ((rc = launch_status("attention_combine"))) return rc;
         }
       }
-      if (lay.n_tail > 0) {  // ragged query tails: single-CTA kernel, tile B skipped
+      if (lay.n_tail > 0) {
         AttnParams q = p;
         q.unit_base = full.reg_pairs * a->n_heads;
         q.n_whole = lay.n_tail;
@@ -1235,10 +1258,14 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
         q.flags = reinterpret_cast<int*>(ws + lay.flags_tail);
         q.flag_pairs = 0;
         LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attn_tc_kernel<true><<<lay.n_tail, AT_THREADS, smem, st>>>(tq, tk, tv, q);
+        attn_tc_kernel<true><<<lay.n_tail, AT_THREADS, smem, ts>>>(tq, tk, tv, q);
         if ((rc = launch_status("attention_tc_window"))) return rc;
-        attn_tc_kernel<false><<<lay.n_tail, AT_THREADS, smem, st>>>(tq, tk, tv, q);
+        attn_tc_kernel<false><<<lay.n_tail, AT_THREADS, smem, ts>>>(tq, tk, tv, q);
         if ((rc = launch_status("attention_tc"))) return rc;
+      }
+      if (ts != st) {
+        LP_CUDA_TRY(cudaEventRecord(fk->join, ts));
+        LP_CUDA_TRY(cudaStreamWaitEvent(st, fk->join, 0));
       }
       return LP_OK;
     }

@@ -77,4 +77,12 @@ __device__ __forceinline__ void rotate_pair(float x, float y, float c, float s, 
   yo = __fadd_rn(__fmul_rn(x, s), __fmul_rn(y, c));
 }
 
+// lp_fork_create handle: a side stream and fork/join events for a launch
+// that runs part of its grid concurrently (GEMM pair + tail split, the
+// attention's ragged query tails).
+struct ForkCtx {
+  cudaStream_t side;
+  cudaEvent_t fork, join;
+};
+
 }  // namespace lp

@@ -54,10 +54,6 @@ __device__ __forceinline__ void a_coords(const GemmParams& p, int kb, int m0, in
   }
 }
 
-struct ForkCtx {
-  cudaStream_t side;
-  cudaEvent_t fork, join;
-};
 
 // Tile raster: groups of LP_GEMM_GROUP row blocks, column-major inside a
 // group, so a wave of ~148 (74 pair) tiles covers a compact block of rows x
@@ -560,7 +556,12 @@ static int launch_gemm_tc(const lp_gemm_args* a, const GemmParams& p, cudaStream
 int fork_create(void** out) {
   LP_CHECK_ARG(out, "lp_fork_create: null argument");
   ForkCtx* f = new ForkCtx();
-  cudaError_t e = cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking);
+  // lowest priority: the side branch's CTAs are scheduled only when no CTA of
+  // the main branch's grid is waiting (they fill its last wave instead of
+  // taking, and fragmenting, SMs a cluster pair of the main grid needs)
+  int least = 0, greatest = 0;
+  cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&f->side, cudaStreamNonBlocking, least);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->join, cudaEventDisableTiming);
   if (e != cudaSuccess) {

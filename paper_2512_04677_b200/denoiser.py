@@ -33,7 +33,7 @@ from . import _lib as L
 from .latent import LatentBlock, TimestepSchedule
 from .model import DenoiserWeights, DeviceWeights, ModelProfile, build_weights, toy_profile
 from .numerics import F32
-from .runtime import Forward, GrowableArena
+from .runtime import Forward, GrowableArena, compute_stream
 
 
 from .errors import TimestepForcingError, raise_compat
@@ -288,7 +288,7 @@ class B200Denoiser:
             if ws is None:
                 fw = Forward(self.dw, n_frames, self._pool.arena)
                 fw.fuse_euler = False  # denoise_block returns the velocity itself
-                stream = torch.cuda.Stream(self.device)
+                stream = compute_stream(self.device)
                 ws = self._ws[t_index] = (fw, stream, min(t_index, self._pool.n_workspaces - 1))
             return ws
 

@@ -41,7 +41,7 @@ from .latent import (Conditions, LatentBlock, PatchVideoCodec, TimestepSchedule,
 from .metrics import MetricsBundle, TimelineEvent, drift_metric, metrics_from_timeline
 from .model import DenoiserWeights, DeviceWeights, ModelProfile, build_weights, toy_profile
 from .numerics import F32, Prng
-from .runtime import Forward, KvArena, h2d, prewarm_torch, wait_event
+from .runtime import Forward, KvArena, compute_stream, h2d, prewarm_torch, wait_event
 from .errors import SinkLockedError, raise_compat
 
 THREADS_ENV = "LIVE_PIPE_THREADS"
@@ -464,7 +464,7 @@ def run_sequential(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResul
     rt = rt or build_runtime(cfg)
     dev = cfg.devices[0]
     with torch.cuda.device(dev):
-        stream = torch.cuda.Stream(dev)
+        stream = compute_stream(dev)
         stages = {j: Stage(cfg, rt, j, dev, stream) for j in range(1, cfg.steps + 1)}
         sink = SinkSlot(rt.conditions.reference.copy(), cfg.sink_delta)
         for st in stages.values():
@@ -588,7 +588,7 @@ def run_tpp(cfg: EngineConfig, rt: Runtime | None = None) -> RolloutResult:
                 L.init_device(a)
                 L.call("lp_peer_enable", a, b)
     abort = torch.zeros(4, dtype=torch.int32, device=f"cuda:{last_dev}")
-    streams = [torch.cuda.Stream(d) for d in devs]
+    streams = [compute_stream(d) for d in devs]
     stages = [Stage(cfg, rt, T - k + 1, devs[k - 1], streams[k - 1]) for k in range(1, T + 1)]
     # link k-1: stage k -> stage k+1 (k = 1..T-1); link T-1: stage T -> decoder
     links = [DeviceLink(nbytes, cfg.link_capacity, devs[k] if k < T else last_dev, abort, cfg.link_timeout_s)
@@ -784,7 +784,7 @@ class StreamingPipeline:
         self.cfg = cfg
         self.rt = rt or build_runtime(cfg)
         self.dev = cfg.devices[0]
-        self.stream = torch.cuda.Stream(self.dev)
+        self.stream = compute_stream(self.dev)
         self.stages = {j: Stage(cfg, self.rt, j, self.dev, self.stream) for j in range(1, cfg.steps + 1)}
         self.sink = SinkSlot(self.rt.conditions.reference.copy(), cfg.sink_delta)
         for st in self.stages.values():

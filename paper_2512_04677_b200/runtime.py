@@ -75,6 +75,13 @@ def h2d(dst: torch.Tensor, src_host, stream) -> torch.Event:
     return ev
 
 
+def compute_stream(device) -> "torch.cuda.Stream":
+    """The stream a forward is launched on: high priority, so the side
+    branches it forks (lp_fork_create streams, the lowest priority) only take
+    SMs its own grids leave idle."""
+    return torch.cuda.Stream(device, priority=-1)
+
+
 class KvArena:
     """K and V of one timestep cache: two [n_layers, rows, d] device tensors."""
 
@@ -504,7 +511,7 @@ class Forward:
                     self._tag("history_noise", "end", stream)
             args = L.AttnArgs(ldt, N, prof.n_heads, prof.head_dim, self.scale, self.q.data_ptr(), kl, vl,
                               self.att.data_ptr(), self.desc_ptr, ar.rows, self.max_keys(), _p(self.attn_ws),
-                              self.attn_ws_bytes)
+                              self.attn_ws_bytes, self.fork)
             if self.probe:
                 self.probe("attention", "begin", stream)
             L.call("lp_attention", C.byref(args), st)

@@ -54,7 +54,7 @@ from .engine import (EngineConfig, EngineConfigError, PipelineInvariantError, Ro
 from .kvcache import SinkSlot, receive_sink
 from .latent import LatentBlock
 from .metrics import TimelineEvent
-from .runtime import prewarm_torch
+from .runtime import compute_stream, prewarm_torch
 from .numerics import F32
 
 # ---------------------------------------------------------------------------
@@ -330,7 +330,7 @@ class DeviceBackend:
 
     def __init__(self, cfg: EngineConfig, rt, role: RankRole, device: int):
         self.cfg, self.rt, self.role, self.device = cfg, rt, role, device
-        self.stream = torch.cuda.Stream(device)
+        self.stream = compute_stream(device)
         self.side = torch.cuda.Stream(device)  # link sends overlap the next block
         self.stages = [Stage(cfg, rt, j, device, self.stream) for j in role.steps]
         prof = cfg.model_profile
