@@ -1156,9 +1156,9 @@ static int64_t flag_bytes(int grid) { return ((int64_t)grid * 4 + 255) / 256 * 2
 
 static AttnPlan plan_pair(int n_q, int n_heads) { return plan_attention(n_q, n_heads, num_sms() / 2, 1.0); }
 
-// The product path: the pair kernel over the units whose 256 rows are all
-// valid, then the ragged query tail of every head (one 128-row tile) on the
-// single-CTA kernel -- a pair would spend a whole M = 256 unit on it.
+// The product path: the pair kernel over every unit; with LP_ATTN_TAIL_SPLIT
+// the ragged query tail of every head (one 128-row tile) runs on the
+// single-CTA kernel instead (forked onto the fork handle's side stream).
 struct PairLayout {
   AttnPlan main;      // regular units only
   int n_tail = 0;     // ragged units (one per head) or 0
@@ -1167,7 +1167,13 @@ struct PairLayout {
 static PairLayout pair_layout(int n_q, int n_heads) {
   PairLayout L;
   const int pairs = (n_q + 2 * AT_M - 1) / (2 * AT_M);
-  const bool ragged = (pairs - 1) * 2 * AT_M + AT_M >= n_q;
+  // Default: the pair grid runs the ragged tails too (a pair spends a whole
+  // M = 256 unit on 72 rows, but the alternatives measured slower: the tails
+  // on the single-CTA kernel after the pair grid 2.20 vs 2.04 ms; forked onto a
+  // low-priority side stream 2.16-2.19 vs 2.01 ms, profiles/r2/attn_ragged_tail_ab.txt).
+  // LP_ATTN_TAIL_SPLIT=1 keeps the split path for A/B.
+  static const bool split_tail = getenv("LP_ATTN_TAIL_SPLIT") != nullptr;
+  const bool ragged = split_tail && (pairs - 1) * 2 * AT_M + AT_M >= n_q;
   const int reg = pairs - (ragged ? 1 : 0);
   if (reg > 0) L.main = plan_pair(reg * 2 * AT_M, n_heads);
   L.n_tail = ragged ? n_heads : 0;
