@@ -1036,6 +1036,384 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
   if (threadIdx.x == 0) p.flags[blockIdx.x] = *win_flag;
 }
 
+// Persistent form of the cluster-pair kernel: one cluster per SM pair walks
+// the work items c, c + G, c + 2G, ... (G = clusters), so the next item's Q,
+// K/V loads and first S MMAs run while the softmax warps finish the previous
+// item's epilogue, and there is no per-item CTA launch, barrier init, TMEM
+// allocation or pipeline fill/drain.  Every ring runs on counters that
+// continue across items (K/V stages, the S/P buffer of global tile g = g & 1
+// and its softmax warpgroup), Q is double-buffered, and the first PV of an
+// item waits for the previous item's epilogue to have read O (o_free).
+struct Attn2pSmem {
+  static constexpr int Q_OFF = 0;                                  // 2 x 32 KB
+  static constexpr int K_OFF = Q_OFF + 2 * AT_TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + A2_KS * A2_KT;
+  static constexpr int BAR_OFF = V_OFF + A2_VS * A2_VT;
+  static constexpr int XM_OFF = BAR_OFF + 512;                     // [128] first-tile max
+  static constexpr int XL_OFF = XM_OFF + AT_M * 4;                 // [2][128] row sums
+  static constexpr int SEG_OFF = XL_OFF + 2 * AT_M * 4;
+  static constexpr int TOTAL = SEG_OFF + 2 * LP_MAX_SEG * 4 + 16 + 1024;
+};
+
+struct Item {  // one work unit or KV piece, as every role derives it
+  int head, pair, piece, t_first, n_tiles;
+};
+__device__ __forceinline__ Item item_of(const AttnParams& p, int it, int nt_total) {
+  Item r;
+  int unit;
+  r.piece = -1;
+  if (it < p.n_whole) {
+    unit = it;
+  } else {
+    const int v = it - p.n_whole;
+    unit = p.n_whole + v / p.split;
+    r.piece = v % p.split;
+  }
+  unit_coords(p, p.unit_base + unit, r.head, r.pair);
+  const int t0 = r.piece < 0 ? 0 : (int)((int64_t)nt_total * r.piece / p.split);
+  const int t1 = r.piece < 0 ? nt_total : (int)((int64_t)nt_total * (r.piece + 1) / p.split);
+  r.t_first = t0;
+  r.n_tiles = t1 - t0;
+  return r;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
+    attn_tc2p_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const AttnParams p, int n_items) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Attn2pSmem::BAR_OFF);
+  uint64_t* q_full = bars;               // [2] leader
+  uint64_t* q_empty = q_full + 2;        // [2] both (multicast commit after an item's last S)
+  uint64_t* k_full = q_empty + 2;        // [KS] leader
+  uint64_t* k_empty = k_full + A2_KS;    // [KS] both
+  uint64_t* v_full = k_empty + A2_KS;    // [VS] leader
+  uint64_t* v_empty = v_full + A2_VS;    // [VS] both
+  uint64_t* s_full = v_empty + A2_VS;    // [2] both
+  uint64_t* s_free = s_full + 2;         // [2] leader: 4 warps x 2 CTAs
+  uint64_t* p_full = s_free + 2;         // [2] leader: 4 warps x 2 CTAs
+  uint64_t* pv_done = p_full + 2;        // [2] both
+  uint64_t* o_done = pv_done + 2;        // both: an item's last PV complete
+  uint64_t* o_free = o_done + 1;         // leader: the epilogue read O (8 warps x 2 CTAs)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
+  int* win_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  float* xm = reinterpret_cast<float*>(smem + Attn2pSmem::XM_OFF);
+  float* xl = reinterpret_cast<float*>(smem + Attn2pSmem::XL_OFF);
+  int* seg_row = reinterpret_cast<int*>(smem + Attn2pSmem::SEG_OFF);
+  int* seg_len = seg_row + LP_MAX_SEG;
+  int* n_seg_s = seg_len + LP_MAX_SEG;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const int c = blockIdx.x >> 1, G = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    plan_segments(p, -1, seg_row, seg_len, n_seg_s);  // the whole range; items take slices of it
+    *win_flag = 0;
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 8);
+      mbar_init(&p_full[i], 8);
+      mbar_init(&pv_done[i], 1);
+    }
+    for (int i = 0; i < A2_KS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < A2_VS; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    mbar_init(o_done, 1);
+    mbar_init(o_free, 16);
+    fence_barrier_init();
+  }
+  cluster_sync_all();
+  if (warp == 1) tmem_alloc_2cta(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int nt_total = n_seg_s[1];
+
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(AT_REG_CTRL));
+  if (warp == 0 || warp == 3) {
+    // ------------------------------------------------ TMA producers (both CTAs)
+    if (elect_one()) {
+      const uint64_t pol = l2_policy_evict_last();
+      uint32_t g = 0;  // global K (warp 0) or V (warp 3) tile counter
+      int k = 0;       // item count of this cluster
+      for (int it = c; it < n_items; it += G, ++k) {
+        const Item im = item_of(p, it, nt_total);
+        const int col0 = im.head * AT_D;
+        TileCursor cur;
+        cur.init(seg_row, seg_len, n_seg_s[0]);
+        cur.skip(im.t_first);
+        if (warp == 0) {
+          const int qb = k & 1;
+          mbar_wait(&q_empty[qb], ((k >> 1) & 1) ^ 1);
+          uint8_t* sq = smem + Attn2pSmem::Q_OFF + qb * AT_TILE_BYTES;
+          const int q0 = im.pair * (2 * AT_M) + (int)rank * AT_M;
+          if (rank == 0) mbar_arrive_expect_tx(&q_full[qb], 2 * AT_TILE_BYTES);
+          tma_load_2d_2sm(sq, &tmQ, &q_full[qb], col0, q0, pol);
+          tma_load_2d_2sm(sq + AT_HALF, &tmQ, &q_full[qb], col0 + 64, q0, pol);
+          for (int t = 0; t < im.n_tiles; ++t, ++g, cur.next()) {
+            const int ks = g % A2_KS;
+            mbar_wait(&k_empty[ks], ((g / A2_KS) & 1) ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&k_full[ks], 2 * A2_KT);
+            uint8_t* sk = smem + Attn2pSmem::K_OFF + ks * A2_KT;
+            const int krow = cur.cur_row() + 64 * (int)rank;
+            tma_load_2d_2sm(sk, &tmK, &k_full[ks], col0, krow, pol);
+            tma_load_2d_2sm(sk + A2_KHALF, &tmK, &k_full[ks], col0 + 64, krow, pol);
+          }
+        } else {
+          for (int t = 0; t < im.n_tiles; ++t, ++g, cur.next()) {
+            const int vs = g % A2_VS;
+            mbar_wait(&v_empty[vs], ((g / A2_VS) & 1) ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&v_full[vs], 2 * A2_VT);
+            tma_load_2d_2sm(smem + Attn2pSmem::V_OFF + vs * A2_VT, &tmV, &v_full[vs], col0 + 64 * (int)rank,
+                            cur.cur_row(), pol);
+          }
+        }
+      }
+    }
+  } else if ((warp == 1 || warp == 2) && rank == 0) {
+    // ------------------------------------------------ MMA issue (leader): S (warp 1), PV (warp 2)
+    constexpr uint32_t IDESC_S = idesc_bf16_f32(2 * AT_M, AT_N);
+    constexpr uint32_t IDESC_O = idesc_bf16_f32(2 * AT_M, AT_D, false, true);
+    uint32_t g = 0;
+    int k = 0;
+    for (int it = c; it < n_items; it += G, ++k) {
+      const Item im = item_of(p, it, nt_total);
+      if (warp == 1) {
+        const int qb = k & 1;
+        const uint32_t sq = smem_u32(smem + Attn2pSmem::Q_OFF + qb * AT_TILE_BYTES);
+        mbar_wait(&q_full[qb], (k >> 1) & 1);
+        for (int t = 0; t < im.n_tiles; ++t, ++g) {
+          if (g >= 2) mbar_wait(&s_free[g & 1], ((g - 2) >> 1) & 1);
+          mbar_wait(&k_full[g % A2_KS], (g / A2_KS) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sk = smem_u32(smem + Attn2pSmem::K_OFF + (g % A2_KS) * A2_KT);
+#pragma unroll
+            for (int kk = 0; kk < AT_D / 16; ++kk)
+              mma_bf16_ss_2cta(tmem_base + (g & 1) * AT_N,
+                               sdesc_kmajor_sw128(sq + (kk >> 2) * AT_HALF + (kk & 3) * 32),
+                               sdesc_kmajor_sw128(sk + (kk >> 2) * A2_KHALF + (kk & 3) * 32), IDESC_S, kk != 0);
+            mma_commit_2cta_mc(&s_full[g & 1]);
+            mma_commit_2cta_mc(&k_empty[g % A2_KS]);
+            if (t == im.n_tiles - 1) mma_commit_2cta_mc(&q_empty[qb]);
+          }
+          __syncwarp();
+        }
+        if (im.n_tiles == 0 && elect_one()) mma_commit_2cta_mc(&q_empty[qb]);
+        __syncwarp();
+      } else {
+        for (int t = 0; t < im.n_tiles; ++t, ++g) {
+          const int b = g & 1;
+          mbar_wait(&v_full[g % A2_VS], (g / A2_VS) & 1);
+          mbar_wait(&p_full[b], (g >> 1) & 1);
+          if (t == 0 && k >= 1) mbar_wait(o_free, (k - 1) & 1);  // the previous item's epilogue read O
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sv = smem_u32(smem + Attn2pSmem::V_OFF + (g % A2_VS) * A2_VT);
+            const uint32_t tp = tmem_base + 384 + b * 64;
+#pragma unroll
+            for (int kk = 0; kk < AT_N / 16; ++kk)
+              mma_bf16_ts_2cta(tmem_base + 256, tp + kk * 8, sdesc_mnmajor_sw128(sv + kk * 16 * 128, A2_VT),
+                               IDESC_O, (t | kk) != 0);
+            mma_commit_2cta_mc(&pv_done[b]);
+            mma_commit_2cta_mc(&v_empty[g % A2_VS]);
+          }
+          __syncwarp();
+        }
+        if (im.n_tiles == 0 && k >= 1) mbar_wait(o_free, (k - 1) & 1);
+        if (elect_one()) mma_commit_2cta_mc(o_done);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ softmax + epilogue (both CTAs)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(AT_REG_SOFTMAX));
+    const int x = (warp - 4) / 4;  // handles global tiles g with g & 1 == x
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t t_s = tmem_base + lane_base + x * AT_N;
+    const uint32_t t_p = tmem_base + lane_base + 384 + x * 64;
+    const uint32_t t_o = tmem_base + lane_base + 256;
+    const float sc = p.scale_log2;
+    const uint64_t sc2 = f32x2(sc, sc);
+    uint32_t g = 0;
+    int k = 0;
+    for (int it = c; it < n_items; it += G, ++k) {
+      const Item im = item_of(p, it, nt_total);
+      const int g0 = (int)g;
+      float m_run = 0.0f, l_run = 0.0f;
+      uint64_t wa2 = 0, wb2 = 0, nm2 = 0;
+      auto set_offset = [&](float m) {
+        m_run = m;
+        const float wa = sc * (1.0f / 192.0f), wb = (127.0f - m_run) * (1.0f / 192.0f);
+        wa2 = f32x2(wa, wa);
+        wb2 = f32x2(wb, wb);
+        nm2 = f32x2(-m_run, -m_run);
+      };
+      // this warpgroup's first tile of the item: the item's tile 0 (it computes
+      // the shared offset) or tile 1 (it waits for the offset)
+      const int first = ((g0 & 1) == x) ? 0 : 1;
+      if (first == 1 && im.n_tiles > 0) {
+        softmax_bar();
+        set_offset(xm[r]);
+      }
+      TileCursor cs;
+      cs.init(seg_row, seg_len, n_seg_s[0]);
+      cs.skip(im.t_first + first);
+      for (int t = first; t < im.n_tiles; t += 2, cs.next(), cs.next()) {
+        const uint32_t gt = (uint32_t)g0 + t;
+        const uint32_t ph = (gt >> 1) & 1;
+        const int nvalid = cs.cur_valid();
+        mbar_wait(&s_full[x], ph);
+        tc_fence_after();
+        uint32_t s[128];
+        tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        tmem_ld32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
+        tmem_ld32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(&s_free[x], 0);
+        if (nvalid < AT_N) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (i >= nvalid) s[i] = __float_as_uint(-INFINITY);
+        }
+        if (t == 0) {
+          float mq[8];
+#pragma unroll
+          for (int kq = 0; kq < 8; ++kq) mq[kq] = fmaxf(__uint_as_float(s[kq]), __uint_as_float(s[kq + 8]));
+#pragma unroll
+          for (int i = 16; i < 128; i += 16)
+#pragma unroll
+            for (int kq = 0; kq < 8; ++kq)
+              mq[kq] = fmaxf(mq[kq], fmaxf(__uint_as_float(s[i + kq]), __uint_as_float(s[i + 8 + kq])));
+          const float mx = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
+                                 fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7]))) * sc;
+          xm[r] = mx;
+          softmax_bar();
+          set_offset(mx);
+        }
+        uint64_t rs2[4];
+#pragma unroll
+        for (int kq = 0; kq < 4; ++kq) rs2[kq] = f32x2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 128; i += 2) {
+          const bool poly = ((i >> 1) & 7) >= 8 - LP_ATTN_POLY_WIN;
+          const uint64_t sv2 = f32x2(__uint_as_float(s[i]), __uint_as_float(s[i + 1]));
+          uint64_t e;
+          if (poly) {
+            e = ex2_poly2_win(sv2, wa2, wb2);
+          } else {
+            const uint64_t a = ffma2(sv2, sc2, nm2);
+            float a0, a1;
+            unpack_f32x2(a, a0, a1);
+            e = f32x2(ex2(a0), ex2(a1));
+          }
+          rs2[(i >> 1) & 3] = fadd2(rs2[(i >> 1) & 3], e);
+          float e0, e1;
+          unpack_f32x2(e, e0, e1);
+          s[i / 2] = pack_bf16(e0, e1);
+        }
+        if (gt >= 2) {  // P_x of global tile gt-2 consumed
+          mbar_wait(&pv_done[x], ph ^ 1);
+          tc_fence_after();
+        }
+        tmem_st32_x(t_p, &s[0]);
+        tmem_st32_x(t_p + 32, &s[32]);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(&p_full[x], 0);
+        float rr[8];
+#pragma unroll
+        for (int kq = 0; kq < 4; ++kq) unpack_f32x2(rs2[kq], rr[2 * kq], rr[2 * kq + 1]);
+        l_run += ((rr[0] + rr[1]) + (rr[2] + rr[3])) + ((rr[4] + rr[5]) + (rr[6] + rr[7]));
+      }
+      g += (uint32_t)im.n_tiles;
+      // epilogue of the item: row sums of both warpgroups, then O / l (or partials)
+      xl[x * AT_M + r] = l_run;
+      softmax_bar();
+      const float l_tot = xl[r] + xl[AT_M + r];
+      const int q0 = im.pair * (2 * AT_M) + (int)rank * AT_M;
+      const int row = q0 + r;
+      const bool valid = row < p.n_q;
+      if (x == 0 && __any_sync(0xffffffffu, valid && !(l_tot < 0x1p64f)) && lane == 0) atomicOr(win_flag, 1);
+      mbar_wait(o_done, k & 1);
+      tc_fence_after();
+      const int col0 = im.head * AT_D;
+      uint32_t v0[32], v1[32];
+      tmem_ld32(t_o + 64 * x, v0);
+      tmem_ld32(t_o + 64 * x + 32, v1);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(o_free, 0);  // O may take the next item's PV
+      if (im.piece >= 0) {
+        const int64_t slot = (int64_t)(it - p.n_whole) * (2 * AT_M) + (int)rank * AT_M + r;
+        float4* o = reinterpret_cast<float4*>(p.part_o + slot * AT_D + 64 * x);
+        const bool any = im.n_tiles > 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          o[q] = any ? make_float4(__uint_as_float(v0[4 * q]), __uint_as_float(v0[4 * q + 1]),
+                                   __uint_as_float(v0[4 * q + 2]), __uint_as_float(v0[4 * q + 3]))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          o[8 + q] = any ? make_float4(__uint_as_float(v1[4 * q]), __uint_as_float(v1[4 * q + 1]),
+                                       __uint_as_float(v1[4 * q + 2]), __uint_as_float(v1[4 * q + 3]))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (x == 0) reinterpret_cast<float2*>(p.part_ml)[slot] = make_float2(any ? m_run : -INFINITY, l_tot);
+      } else if (valid) {
+        const float inv_l = l_tot > 0.0f ? 1.0f / l_tot : 0.0f;
+        uint4* o = reinterpret_cast<uint4*>(p.out + (int64_t)row * p.ldo + col0 + 64 * x);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          o[q] = make_uint4(pack_bf16(__uint_as_float(v0[8 * q]) * inv_l, __uint_as_float(v0[8 * q + 1]) * inv_l),
+                            pack_bf16(__uint_as_float(v0[8 * q + 2]) * inv_l, __uint_as_float(v0[8 * q + 3]) * inv_l),
+                            pack_bf16(__uint_as_float(v0[8 * q + 4]) * inv_l, __uint_as_float(v0[8 * q + 5]) * inv_l),
+                            pack_bf16(__uint_as_float(v0[8 * q + 6]) * inv_l, __uint_as_float(v0[8 * q + 7]) * inv_l));
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          o[4 + q] =
+              make_uint4(pack_bf16(__uint_as_float(v1[8 * q]) * inv_l, __uint_as_float(v1[8 * q + 1]) * inv_l),
+                         pack_bf16(__uint_as_float(v1[8 * q + 2]) * inv_l, __uint_as_float(v1[8 * q + 3]) * inv_l),
+                         pack_bf16(__uint_as_float(v1[8 * q + 4]) * inv_l, __uint_as_float(v1[8 * q + 5]) * inv_l),
+                         pack_bf16(__uint_as_float(v1[8 * q + 6]) * inv_l, __uint_as_float(v1[8 * q + 7]) * inv_l));
+      }
+      softmax_bar();  // win_flag complete; xl free for the next item
+      if (warp == 4 && lane == 0) {
+        p.flags[2 * it + rank] = *win_flag;
+        *win_flag = 0;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2cta(tmem_base, 512);
+  }
+}
+
 // Merge the KV-range partials of the split units in piece order:
 // O = sum_s 2^(m_s - m) O_s / sum_s 2^(m_s - m) l_s (one warp per query row).
 __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnParams p) {
@@ -1075,6 +1453,7 @@ int preload_attn_tc() {
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_tc_kernel<true>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_tc_kernel<false>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_tc2_kernel));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_tc2p_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_combine_kernel));
   return LP_OK;
 }
@@ -1243,10 +1622,19 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
         CUtensorMap tk2;  // this CTA's 64 keys of a tile
         rc = make_tmap_bf16_2d(&tk2, a->k_arena, (uint64_t)a->arena_rows, (uint64_t)d, (uint64_t)d, 64, 64);
         if (rc) return rc;
-        LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Attn2Smem::TOTAL));
-        attn_tc2_kernel<<<2 * pm.grid(), AT_THREADS, Attn2Smem::TOTAL, st>>>(tq, tk2, tv, q);
-        if ((rc = launch_status("attention_tc2"))) return rc;
+        static const bool persist = getenv("LP_ATTN_NONPERSIST") == nullptr;
+        if (persist) {  // one cluster per SM pair walks the items
+          const int clusters = std::min(pm.grid(), std::max(1, num_sms() / 2));
+          LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           Attn2pSmem::TOTAL));
+          attn_tc2p_kernel<<<2 * clusters, AT_THREADS, Attn2pSmem::TOTAL, st>>>(tq, tk2, tv, q, pm.grid());
+          if ((rc = launch_status("attention_tc2p"))) return rc;
+        } else {
+          LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           Attn2Smem::TOTAL));
+          attn_tc2_kernel<<<2 * pm.grid(), AT_THREADS, Attn2Smem::TOTAL, st>>>(tq, tk2, tv, q);
+          if ((rc = launch_status("attention_tc2"))) return rc;
+        }
         attn_tc_kernel<false><<<pm.grid(), AT_THREADS, smem, st>>>(tq, tk, tv, q);  // rerun flagged units
         if ((rc = launch_status("attention_tc"))) return rc;
         if (pm.n_whole < pm.n_units) {

@@ -4,8 +4,8 @@ mkdir -p $OUT
 timeout 300 python -m pytest tests/test_gpu_attn.py -x -q --timeout 120 > $OUT/pytest_attn.log 2>&1
 echo "rc=$?" >> $OUT/pytest_attn.log
 if grep -q " passed" $OUT/pytest_attn.log && ! grep -q "failed\|Timeout\|rc=[1-9]" $OUT/pytest_attn.log; then
-  for v in default inpair single default inpair; do
-    if [ $v = default ]; then E=""; elif [ $v = single ]; then E="LP_ATTN_SINGLE=1"; elif [ $v = inpair ]; then E="LP_ATTN_RAGGED_IN_PAIR=1"; else E="LIVEPIPE_LIB=$PWD/paper_2512_04677_b200/$v.so"; fi
+  for v in default nonpersist default nonpersist; do
+    if [ $v = default ]; then E=""; elif [ $v = single ]; then E="LP_ATTN_SINGLE=1"; elif [ $v = nonpersist ]; then E="LP_ATTN_NONPERSIST=1"; else E="LIVEPIPE_LIB=$PWD/paper_2512_04677_b200/$v.so"; fi
     env $E timeout 420 python bench.py --no-cpu-baseline --no-decode --steps 4 > $OUT/bench_$v.json 2> $OUT/bench_$v.err
     python -c "import json; d=json.loads(open('$OUT/bench_$v.json').read().strip().splitlines()[-1]); print('$v', round(d['value'],3), d['clocks']['sm_mhz'], {k: round(x['avg_ms'],4) for k,x in d['kernels'].items()})" >> $OUT/summary.txt 2>&1
   done
