@@ -1470,6 +1470,14 @@ struct AttnPlan {
   int grid() const { return n_whole + (int)pieces(); }
 };
 
+// Static round-robin assignment (the persistent kernel: cluster c runs items
+// c, c + slots, ...): the largest per-slot sum.
+static double makespan_rr(const std::vector<double>& costs, int slots) {
+  std::vector<double> t(slots, 0.0);
+  for (size_t i = 0; i < costs.size(); ++i) t[i % slots] += costs[i];
+  return *std::max_element(t.begin(), t.end());
+}
+
 static double makespan(const std::vector<double>& costs, int sms) {
   std::priority_queue<double, std::vector<double>, std::greater<double>> q;
   for (int i = 0; i < sms; ++i) q.push(0.0);
@@ -1487,11 +1495,11 @@ static double makespan(const std::vector<double>& costs, int sms) {
 // kernel); c_rag = relative cost of a unit whose second 128-row tile is empty
 // (0.6 single-CTA: its MMAs and softmax are skipped; 1.0 for a pair, whose
 // M = 256 MMAs run regardless).
-static AttnPlan plan_attention(int n_q, int n_heads, int sms, double c_rag = 0.6) {
+static AttnPlan plan_attention(int n_q, int n_heads, int sms, double c_rag = 0.6, bool rr = false) {
   static std::mutex mu;
-  static std::map<std::tuple<int, int, int, int>, AttnPlan> cache;
+  static std::map<std::tuple<int, int, int, int, bool>, AttnPlan> cache;
   std::lock_guard<std::mutex> lock(mu);
-  auto key = std::make_tuple(n_q, n_heads, sms, (int)(c_rag * 100));
+  auto key = std::make_tuple(n_q, n_heads, sms, (int)(c_rag * 100), rr);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   AttnPlan pl;
@@ -1514,7 +1522,7 @@ static AttnPlan plan_attention(int n_q, int n_heads, int sms, double c_rag = 0.6
       for (int u = 0; u < n_whole; ++u) costs.push_back(cost(u) + eps);
       for (int u = n_whole; u < pl.n_units; ++u)
         for (int s = 0; s < split; ++s) costs.push_back(cost(u) / split + eps);
-      double t = makespan(costs, sms) + (n_split ? 0.05 : 0.0);
+      double t = (rr ? makespan_rr(costs, sms) : makespan(costs, sms)) + (n_split ? 0.05 : 0.0);
       if (t < best - 1e-9) {
         best = t;
         bp.n_whole = n_whole;
@@ -1533,7 +1541,13 @@ static AttnPlan plan_attention(int n_q, int n_heads, int sms, double c_rag = 0.6
 static int64_t partial_bytes(const AttnPlan& pl) { return pl.pieces() * (2 * AT_M) * (AT_D + 2) * 4; }
 static int64_t flag_bytes(int grid) { return ((int64_t)grid * 4 + 255) / 256 * 256; }
 
-static AttnPlan plan_pair(int n_q, int n_heads) { return plan_attention(n_q, n_heads, num_sms() / 2, 1.0); }
+static bool persistent_attention() {
+  static const bool persist = getenv("LP_ATTN_NONPERSIST") == nullptr;
+  return persist;
+}
+static AttnPlan plan_pair(int n_q, int n_heads) {
+  return plan_attention(n_q, n_heads, num_sms() / 2, 1.0, persistent_attention());
+}
 
 // The product path: the pair kernel over every unit; with LP_ATTN_TAIL_SPLIT
 // the ragged query tail of every head (one 128-row tile) runs on the
@@ -1622,8 +1636,7 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
         CUtensorMap tk2;  // this CTA's 64 keys of a tile
         rc = make_tmap_bf16_2d(&tk2, a->k_arena, (uint64_t)a->arena_rows, (uint64_t)d, (uint64_t)d, 64, 64);
         if (rc) return rc;
-        static const bool persist = getenv("LP_ATTN_NONPERSIST") == nullptr;
-        if (persist) {  // one cluster per SM pair walks the items
+        if (persistent_attention()) {  // one cluster per SM pair walks the items
           const int clusters = std::min(pm.grid(), std::max(1, num_sms() / 2));
           LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            Attn2pSmem::TOTAL));
