@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LIVEPIPE_LIB") or os.path.join(HERE, "liblivepipe_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "livepipe_b200.h")
 
-ABI_VERSION = 6  # LP_ABI_VERSION in include/livepipe_b200.h
+ABI_VERSION = 7  # LP_ABI_VERSION in include/livepipe_b200.h
 LP_OK, LP_EINVAL, LP_ECUDA, LP_EUNSUPPORTED, LP_ETIMEOUT, LP_EABORT = range(6)
 LP_F32, LP_BF16 = 0, 1
 EPI_STORE, EPI_RELU, EPI_GELU, EPI_RESID, EPI_QKV, EPI_EULER = range(6)
@@ -58,7 +58,8 @@ class EulerEpi(C.Structure):
 
 
 class ConvTaps(C.Structure):
-    _fields_ = [("n_taps", i32), ("cin", i32), ("tap_row", i32 * 27)]
+    _fields_ = [("n_taps", i32), ("cin", i32), ("tap_row", i32 * 27), ("frames", i32), ("height", i32),
+                ("width", i32)]
 
 
 class GemmArgs(C.Structure):

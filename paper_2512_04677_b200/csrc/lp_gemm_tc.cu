@@ -41,6 +41,7 @@ struct GemmParams {
   // columns (kb % conv_kpt) * GBK; conv_kpt = 0 for a plain GEMM
   int conv_kpt;
   int tap_row[27];
+  int conv_t, conv_h, conv_w;  // halo conv (conv_tc_kernel): interior frames, height, width
 };
 
 __device__ __forceinline__ void a_coords(const GemmParams& p, int kb, int m0, int& col, int& row) {
@@ -372,6 +373,166 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Halo-tile causal 3x3x3 convolution (the decode stage's VAE stand-in):
+// output tile = 8 image rows x 16 pixels of one frame (128 TMEM lanes) x BN
+// channels.  For every (dt, dx) and 64-channel chunk one 4-D TMA box brings
+// the 10 x 16-pixel window (rows y0-1 .. y0+8 of the bordered layout) whose
+// three 8-row views at 16-row offsets are the A operands of the dy = -1, 0, +1
+// taps -- 2.4x less A traffic than one row-shifted box per tap -- plus the
+// three taps' weight chunks.  Frames before 0 (causal padding) and the window
+// rows past the last frame are TMA zero fill; the bordered layout supplies the
+// spatial padding.  Same warp roles and double-buffered TMEM accumulator as
+// gemm_tc_kernel; the epilogue maps lane r to pixel (y0 + r/16, x0 + r%16).
+template <int BN>
+struct ConvSmem {
+  static constexpr int A_BYTES = 10 * 16 * 128;  // 20 KB window
+  static constexpr int B_BYTES = 3 * BN * GBK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN >= 128 ? 3 : 4;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(G_THREADS, 1)
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const GemmParams p) {
+  using SM = ConvSmem<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+  uint64_t* empty = full + SM::STAGES;
+  uint64_t* tfull = empty + SM::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int T = p.conv_t, H = p.conv_h, W = p.conv_w, cin = p.conv_kpt * GBK;
+  const int ty = (H + 7) / 8, tx = (W + 15) / 16, tiles_n = p.n / BN;
+  const int num_tiles = T * ty * tx * tiles_n;
+  const int num_kb = 9 * p.conv_kpt;  // (dt, dx) x 64-channel chunks; 3 dy taps per block
+  auto coords = [&](int tile, int& t, int& y0, int& x0, int& n0) {
+    n0 = (tile % tiles_n) * BN;  // N innermost: consecutive tiles share the A windows in L2
+    int r = tile / tiles_n;
+    x0 = (r % tx) * 16;
+    r /= tx;
+    y0 = (r % ty) * 8;
+    t = r / ty;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < SM::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    fence_barrier_init();
+  }
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int t, y0, x0, n0;
+        coords(tile, t, y0, x0, n0);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          const int tdx = kb / p.conv_kpt, kc = (kb - tdx * p.conv_kpt) * GBK;
+          const int dt = tdx / 3 - 2, dx = tdx % 3 - 1;
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * SM::STAGE_BYTES;
+          uint8_t* sb = sa + SM::A_BYTES;
+          mbar_arrive_expect_tx(&full[stage], SM::STAGE_BYTES);
+          // window: bordered columns x0+1+dx .. +15, bordered rows y0 .. y0+9, frame t+dt
+          tma_load_4d(sa, &tmA, &full[stage], kc, x0 + 1 + dx, y0, t + dt);
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy)  // tap (dt, dy-1, dx) weights: K chunk of tap index (dt+2)*9 + dy*3 + dx+1
+            tma_load_2d(sb + dy * BN * GBK * 2, &tmB, &full[stage], ((dt + 2) * 9 + dy * 3 + dx + 1) * cin + kc,
+                        n0);
+          if (++stage == SM::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t IDESC = idesc_bf16_f32(GBM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t aphase = (local >> 1) & 1;
+      mbar_wait(&tempty[acc], aphase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_u32(smem + stage * SM::STAGE_BYTES);
+          const uint32_t sb = sa + SM::A_BYTES;
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy) {
+            const uint64_t da = sdesc_kmajor_sw128(sa + dy * 16 * 128);  // window rows 16*dy ..: the dy tap
+            const uint64_t db = sdesc_kmajor_sw128(sb + dy * BN * GBK * 2);
+#pragma unroll
+            for (int k = 0; k < GBK / 16; ++k)
+              mma_bf16_ss(d_tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), IDESC, (kb | dy | k) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (kb == num_kb - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == SM::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    int local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t aphase = (local >> 1) & 1;
+      int t, y0, x0, n0;
+      coords(tile, t, y0, x0, n0);
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const int r = quarter * 32 + lane, yy = y0 + r / 16, xx = x0 + r % 16;
+      const bool valid = yy < H && xx < W;
+      const int row = (t * (H + 2) + yy + 1) * (W + 2) + xx + 1;
+      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      gemm_epilogue_tile<BN>(p, valid ? row : 0, valid, tbase, n0, half, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // 2-CTA variant (cluster pair, tcgen05.mma.cta_group::2): tile 256 x BN per
 // pair, each CTA loads its 128 rows of A and its BN/2 rows of B, the leader
 // issues M = 256 MMAs whose accumulator halves land in each CTA's TMEM.  Per
@@ -537,6 +698,25 @@ static int launch_gemm_tc2(const lp_gemm_args* a, const GemmParams& p, cudaStrea
 }
 
 template <int BN>
+static int launch_conv_tc(const lp_gemm_args* a, const GemmParams& p, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  const uint64_t dims[4] = {(uint64_t)p.conv_kpt * GBK, (uint64_t)p.conv_w + 2, (uint64_t)p.conv_h + 2,
+                            (uint64_t)p.conv_t};
+  const uint32_t box[4] = {GBK, 16, 10, 1};
+  int rc = make_tmap_bf16_4d(&ta, a->a, dims, box);
+  if (rc) return rc;
+  rc = make_tmap_bf16_2d(&tb, a->w, (uint64_t)a->n, (uint64_t)a->k, (uint64_t)a->ldw, BN, GBK);
+  if (rc) return rc;
+  const int tiles = p.conv_t * ((p.conv_h + 7) / 8) * ((p.conv_w + 15) / 16) * (a->n / BN);
+  const int grid = std::min(tiles, std::max(1, num_sms()));
+  const int smem = ConvSmem<BN>::TOTAL;
+  auto kern = conv_tc_kernel<BN>;
+  LP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<grid, G_THREADS, smem, st>>>(ta, tb, p);
+  return launch_status("conv_tc");
+}
+
+template <int BN>
 static int launch_gemm_tc(const lp_gemm_args* a, const GemmParams& p, cudaStream_t st) {
   CUtensorMap ta, tb;
   const uint64_t a_cols = p.conv_kpt ? (uint64_t)p.conv_kpt * GBK : (uint64_t)a->k;  // conv: A is [rows, cin]
@@ -588,6 +768,8 @@ int preload_gemm_tc() {
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, gemm_tc_kernel<128>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, gemm_tc_kernel<256>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, gemm_tc2_kernel<256>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, conv_tc_kernel<128>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, conv_tc_kernel<64>));
   return LP_OK;
 }
 
@@ -661,6 +843,12 @@ int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
     LP_CHECK_ARG(a->lda == cv.cin, "gemm_tc: conv A is [rows, cin] (lda == cin)");
     p.conv_kpt = cv.cin / GBK;
     for (int t = 0; t < cv.n_taps; ++t) p.tap_row[t] = cv.tap_row[t];
+    p.conv_t = cv.frames, p.conv_h = cv.height, p.conv_w = cv.width;
+    if (cv.n_taps == 27 && cv.frames > 0 && cv.height > 0 && cv.width > 0 && getenv("LP_CONV_ROWSHIFT") == nullptr) {
+      LP_CHECK_ARG((int64_t)cv.frames * (cv.height + 2) * (cv.width + 2) == a->m, "gemm_tc: conv geometry vs m");
+      if (a->n % 128 == 0) return launch_conv_tc<128>(a, p, st);
+      if (a->n % 64 == 0) return launch_conv_tc<64>(a, p, st);
+    }
     // single-CTA tiles: the A box of a tap is one row-shifted 128-row window
     if (a->n % 256 == 0) return launch_gemm_tc<256>(a, p, st);
     if (a->n % 128 == 0) return launch_gemm_tc<128>(a, p, st);
@@ -750,6 +938,20 @@ int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_
                         CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(LP_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return LP_OK;
+}
+
+int make_tmap_bf16_4d(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint32_t box[4]) {
+  if (!g_encode) return fail(LP_EINVAL, "TMA not initialised (call lp_init)");
+  cuuint64_t d[4] = {dims[0], dims[1], dims[2], dims[3]};
+  cuuint64_t strides[3] = {dims[0] * 2, dims[0] * dims[1] * 2, dims[0] * dims[1] * dims[2] * 2};
+  cuuint32_t b[4] = {box[0], box[1], box[2], box[3]};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUtensorMapSwizzle sw = box[0] * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), d, strides, b, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LP_ECUDA, "cuTensorMapEncodeTiled (4-D) failed: " + std::to_string((int)r));
   return LP_OK;
 }
 

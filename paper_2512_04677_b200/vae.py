@@ -13,11 +13,13 @@ nearest x2 upsampling in space with x2 in time twice, conv_out to RGB), so a
 384, 192, 128 where the Wan decoder uses 384, 384, 192, 96.
 
 Layout: every activation is [T][H+2][W+2][C] rows with a one-pixel zero
-border; a 3x3x3 causal conv is one lp_gemm whose K walks the 27 taps as
-constant row shifts of the A operand (lp_conv_taps) -- TMA zero-fills the
-rows before frame 0 (causal temporal padding) and the border pixels supply
-the spatial padding.  Conv outputs on border rows are don't-care; the
-norm / cast kernels that build the next conv input write the border as 0.
+border; a 3x3x3 causal conv is one lp_gemm whose K walks the 27 taps
+(lp_conv_taps): with the geometry given, as halo tiles of 8 x 16 pixels whose
+10 x 16 window per (dt, dx) feeds the three dy taps (conv_tc_kernel), else as
+constant row shifts of the A operand -- TMA zero-fills the frames before 0
+(causal temporal padding) and the border pixels supply the spatial padding.
+Conv outputs on border rows are don't-care; the norm / cast kernels that
+build the next conv input write the border as 0.
 """
 
 from __future__ import annotations
@@ -108,10 +110,10 @@ class VaeDecoder:
     # -- launches ---------------------------------------------------------
     def _conv(self, st: int, a: torch.Tensor, t: int, h: int, w: int, cin: int, wt: torch.Tensor, cout: int,
               out: torch.Tensor, resid: bool) -> None:
-        key = (h, w, cin)
+        key = (t, h, w, cin)
         ct = self._taps.get(key)
-        if ct is None:
-            ct = self._taps[key] = L.ConvTaps(27, cin, (C.c_int32 * 27)(*tap_rows(h, w)))
+        if ct is None:  # with the geometry the library runs the halo-tile conv kernel
+            ct = self._taps[key] = L.ConvTaps(27, cin, (C.c_int32 * 27)(*tap_rows(h, w)), t, h, w)
         args = L.GemmArgs()
         args.in_dtype, args.out_dtype = L.LP_BF16, L.LP_F32
         args.epilogue = L.EPI_RESID if resid else L.EPI_STORE

@@ -20,7 +20,7 @@ def test_library_exports_every_header_symbol():
     assert len(syms) >= 20
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.lp_abi_version() == L.ABI_VERSION == 6
+    assert lib.lp_abi_version() == L.ABI_VERSION == 7
 
 
 def test_ctypes_signatures_cover_header():

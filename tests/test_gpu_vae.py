@@ -45,8 +45,12 @@ def _conv_ref(x, k):
     return F.conv3d(F.pad(x, (1, 1, 1, 1, 2, 0)), k)
 
 
-@pytest.mark.parametrize("t,h,w,cin,cout", [(3, 6, 9, 64, 64), (4, 10, 7, 128, 256), (2, 5, 5, 192, 128)])
-def test_conv_taps_gemm_matches_conv3d(t, h, w, cin, cout):
+@pytest.mark.parametrize("halo", [False, True])
+@pytest.mark.parametrize("t,h,w,cin,cout", [(3, 6, 9, 64, 64), (4, 10, 7, 128, 256), (2, 5, 5, 192, 128),
+                                           (3, 17, 35, 64, 192), (2, 16, 32, 128, 384)])
+def test_conv_taps_gemm_matches_conv3d(t, h, w, cin, cout, halo):
+    # row-shifted taps (geometry 0) and halo tiles (geometry given): ragged
+    # 8 x 16 tiles at the right / bottom edges, causal frames, N = 64..384
     g = torch.Generator(device=DEV).manual_seed(t * 100 + cin)
     rows = t * (h + 2) * (w + 2)
     a = torch.randn((rows, cin), generator=g, device=DEV).to(torch.bfloat16)
@@ -57,7 +61,7 @@ def test_conv_taps_gemm_matches_conv3d(t, h, w, cin, cout):
     a4[:, :, -1] = 0
     wt = (torch.randn((cout, 27 * cin), generator=g, device=DEV) / np.sqrt(27 * cin)).to(torch.bfloat16)
     out = torch.full((rows, cout), float("nan"), device=DEV)
-    ct = L.ConvTaps(27, cin, (C.c_int32 * 27)(*tap_rows(h, w)))
+    ct = L.ConvTaps(27, cin, (C.c_int32 * 27)(*tap_rows(h, w)), *((t, h, w) if halo else (0, 0, 0)))
     args = L.GemmArgs()
     args.in_dtype, args.out_dtype, args.epilogue = L.LP_BF16, L.LP_F32, L.EPI_STORE
     args.m, args.n, args.k = rows, cout, 27 * cin
