@@ -162,7 +162,7 @@ def run_reference(args):
     n_tok = 3 * prof.tokens_per_frame
     n_kv = prof.tokens_per_frame + 5 * n_tok
     k, w = max(1, args.steps), max(0, args.warmup)
-    per = min(6.0, 150.0 / k)
+    per = min(2.0, 40.0 / k)  # target seconds of matmul per sample (each sample's wall time is ~3x: process fan-out)
     for _ in range(w):
         cpu_baseline(prof, n_tok, n_kv, 4, target_s=0.5)
     vals, walls, cb = [], [], None
