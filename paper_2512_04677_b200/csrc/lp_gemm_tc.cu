@@ -411,13 +411,17 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   const int ty = (H + 7) / 8, tx = (W + 15) / 16, tiles_n = p.n / BN;
   const int num_tiles = T * ty * tx * tiles_n;
   const int num_kb = 9 * p.conv_kpt;  // (dt, dx) x 64-channel chunks; 3 dy taps per block
+  // order: N fastest, then time, then x, then y -- the tiles in flight share
+  // their A windows in L2 across output channels and across the three
+  // frames each causal tap reads (frame-major order re-read every frame
+  // from DRAM three times: 7.5 GB per stage-3 conv)
   auto coords = [&](int tile, int& t, int& y0, int& x0, int& n0) {
-    n0 = (tile % tiles_n) * BN;  // N innermost: consecutive tiles share the A windows in L2
+    n0 = (tile % tiles_n) * BN;
     int r = tile / tiles_n;
+    t = r % T;
+    r /= T;
     x0 = (r % tx) * 16;
-    r /= tx;
-    y0 = (r % ty) * 8;
-    t = r / ty;
+    y0 = (r / tx) * 8;
   };
 
   if (warp == 0 && lane == 0) {
