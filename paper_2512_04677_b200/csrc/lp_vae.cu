@@ -68,6 +68,53 @@ __global__ void vae_norm_silu_kernel(const float* __restrict__ h, const float* _
   }
 }
 
+// Same, float4 per lane (C a multiple of 128: 128 -> 1, 256 -> 2, 384 -> 3
+// float4 per lane): one 16-byte load and one 8-byte store per 4 channels.
+template <int PER4>
+__global__ void vae_norm_silu4_kernel(const float* __restrict__ h, const float* __restrict__ gamma, int T, int H,
+                                      int W, int C, int mode, float eps, __nv_bfloat16* __restrict__ out) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int64_t rows = (int64_t)T * (H + 2) * (W + 2);
+  if (row >= rows) return;
+  const int xx = (int)(row % (W + 2)), yy = (int)((row / (W + 2)) % (H + 2));
+  uint2* o = reinterpret_cast<uint2*>(out + row * C);
+  if (xx == 0 || yy == 0 || xx == W + 1 || yy == H + 1) {
+#pragma unroll
+    for (int k = 0; k < PER4; ++k) o[k * 32 + lane] = make_uint2(0u, 0u);
+    return;
+  }
+  const float4* x = reinterpret_cast<const float4*>(h + row * C);
+  float4 v[PER4];
+  float ss = 0.0f;
+#pragma unroll
+  for (int k = 0; k < PER4; ++k) {
+    v[k] = x[k * 32 + lane];
+    ss += (v[k].x * v[k].x + v[k].y * v[k].y) + (v[k].z * v[k].z + v[k].w * v[k].w);
+  }
+  float scale = 1.0f;
+  if (mode == 1) {
+#pragma unroll
+    for (int s = 16; s; s >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, s);
+    scale = rsqrtf(ss / C + eps);
+  }
+#pragma unroll
+  for (int k = 0; k < PER4; ++k) {
+    float y[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+    if (mode == 1) {
+      const float4 g = reinterpret_cast<const float4*>(gamma)[k * 32 + lane];
+      const float gg[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float t = y[e] * scale * gg[e];
+        y[e] = t / (1.0f + __expf(-t));
+      }
+    }
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(y[0], y[1]), p1 = __floats2bfloat162_rn(y[2], y[3]);
+    o[k * 32 + lane] = make_uint2(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1));
+  }
+}
+
 // Nearest upsampling x2 in space (and x ft in time) between bordered layouts:
 // in [T][H+2][W+2][C] -> out [T*ft][2H+2][2W+2][C], 8 channels per thread.
 __global__ void vae_upsample_kernel(const __nv_bfloat16* __restrict__ in, int T, int H, int W, int C, int ft,
@@ -114,6 +161,9 @@ int preload_vae() {
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, vae_norm_silu_kernel<4>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, vae_norm_silu_kernel<8>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, vae_norm_silu_kernel<16>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, vae_norm_silu4_kernel<1>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, vae_norm_silu4_kernel<2>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, vae_norm_silu4_kernel<3>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, vae_upsample_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, vae_frames_kernel));
   return LP_OK;
@@ -132,6 +182,15 @@ int vae_norm_silu(const float* h, const float* gamma, int T, int H, int W, int C
   const int64_t rows = (int64_t)T * (H + 2) * (W + 2);
   const unsigned blocks = nblocks(rows, 8);
   auto* o = (__nv_bfloat16*)out;
+  if (C == 128 || C == 256 || C == 384) {
+    if (C == 128)
+      vae_norm_silu4_kernel<1><<<blocks, 256, 0, st>>>(h, gamma, T, H, W, C, mode, eps, o);
+    else if (C == 256)
+      vae_norm_silu4_kernel<2><<<blocks, 256, 0, st>>>(h, gamma, T, H, W, C, mode, eps, o);
+    else
+      vae_norm_silu4_kernel<3><<<blocks, 256, 0, st>>>(h, gamma, T, H, W, C, mode, eps, o);
+    return launch_status("vae_norm_silu");
+  }
   if (C <= 64)
     vae_norm_silu_kernel<2><<<blocks, 256, 0, st>>>(h, gamma, T, H, W, C, mode, eps, o);
   else if (C <= 128)
