@@ -79,7 +79,9 @@ def test_tpp_bitwise_equals_sequential(name, capacity):
 
 
 def test_drop_in_matches_engine_bitwise(toy):
-    # the reference engine loop driven through the drop-in API == our fast path
+    # a restatement of the reference engine's run_sequential loop (engine.py:255-285)
+    # driven through the drop-in API == our fast path (the unmodified reference
+    # engine itself runs on the drop-in in tests/test_gpu_reference_engine.py)
     cfg = lp.EngineConfig(mode="sequential", steps=4, blocks=3)
     rt = lp.build_runtime(cfg)
     dn = lp.B200Denoiser(rt.weights, rt.schedule, precision="fp32")

@@ -209,7 +209,7 @@ def test_1p3b_shape_tpp_bitwise_equals_sequential():
 
 
 def test_drop_in_denoiser_wan_bf16_matches_engine():
-    # the reference engine loop (engine.py:255-285) driven through the
+    # a restatement of the reference engine loop (engine.py:255-285) driven through the
     # drop-in B200Denoiser on the Wan profile in bf16, against the fast
     # engine: the drop-in keeps its entries in its own K/V pool, so the
     # tcgen05 attention visits the same keys in a different arena order
