@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LP_ABI_VERSION 7
+#define LP_ABI_VERSION 8
 
 /* status codes */
 #define LP_OK 0
@@ -192,6 +192,10 @@ typedef struct lp_gemm_args {
                              rows as single-CTA tiles on the handle's side
                              stream, concurrently (fork/join events on
                              `stream`; graph-capture safe)                   */
+  float* row_stats;       /* RESID only, or NULL: LayerNorm statistics of the
+                             updated h rows for the next norm (AdaLN) pass,
+                             one (mean, M2) float pair per 32-column chunk,
+                             [m][n/32] (ABI v8; feeds lp_norm_mod_stats)     */
 } lp_gemm_args;
 LP_API int lp_gemm(const lp_gemm_args* args, void* stream);
 
@@ -266,6 +270,14 @@ LP_API int lp_norm_mod(const float* h, int rows, int d, int mode, float eps,
                 const float* shift, const float* scale, void* out, int out_dtype,
                 void* stream);
 
+/* lp_norm_mod (mode 1 or 2) with the row statistics taken from `stats`, the
+   per-32-column (mean, M2) partials a RESID lp_gemm wrote for these h rows
+   (lp_gemm_args.row_stats, [rows][d/32] float pairs): the pre-LN + AdaLN of
+   denoiser.py's Wan profile with its reduction fused into the producing
+   GEMM's epilogue, leaving one streaming apply pass.  d % 32 == 0.        */
+LP_API int lp_norm_mod_stats(const float* h, const float* stats, int rows, int d, int mode, float eps,
+                      const float* shift, const float* scale, void* out, int out_dtype, void* stream);
+
 /* Sink K/V at the block's sink position (denoiser.py:187-190, :246-249) for
    n_layers layers in one launch: k_raw/v_raw fp32 [S, d] per layer
    (raw_layer_stride elements apart) are the un-rotated projections of the
@@ -337,8 +349,10 @@ LP_API int lp_oracle_step(const float* x, const float* target, float s, float dt
    [seg_row[s], +seg_len[s]) = arena rows [src_row[s], +seg_len[s])
    + desc->sigma * z (the stored ring rows are never modified).  z comes from
    `noise` (host-generated in the reference draw order,
-   [entry][kv][layer][rows][d], parity runs) or, when noise == NULL, from the
-   device Philox4x32 stream keyed by desc->noise_key (perf runs).
+   [entry][kv][layer][rows][d], parity runs) or, when noise == NULL, from a
+   device counter-hash stream keyed by desc->noise_key and (layer, kv, entry)
+   (perf runs; bf16: exact Box-Muller with the sines on the FMA pipe, fp32:
+   Philox4x32-7).
    max_rows bounds the history rows (grid size).                            */
 LP_API int lp_history_noise(void* arena, int dtype, int d, const float* noise, int n_layers, int layer,
                      int kv, const lp_block_desc* desc, int max_rows, void* stream);

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LIVEPIPE_LIB") or os.path.join(HERE, "liblivepipe_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "livepipe_b200.h")
 
-ABI_VERSION = 7  # LP_ABI_VERSION in include/livepipe_b200.h
+ABI_VERSION = 8  # LP_ABI_VERSION in include/livepipe_b200.h
 LP_OK, LP_EINVAL, LP_ECUDA, LP_EUNSUPPORTED, LP_ETIMEOUT, LP_EABORT = range(6)
 LP_F32, LP_BF16 = 0, 1
 EPI_STORE, EPI_RELU, EPI_GELU, EPI_RESID, EPI_QKV, EPI_EULER = range(6)
@@ -66,7 +66,7 @@ class GemmArgs(C.Structure):
     _fields_ = [("in_dtype", i32), ("out_dtype", i32), ("epilogue", i32), ("m", i32), ("n", i32),
                 ("k", i32), ("lda", i64), ("ldw", i64), ("ldc", i64), ("a", vp), ("w", vp), ("c", vp),
                 ("bias", vp), ("gate", vp), ("qkv", C.POINTER(QkvEpi)), ("euler", C.POINTER(EulerEpi)),
-                ("conv", C.POINTER(ConvTaps)), ("fork", vp)]
+                ("conv", C.POINTER(ConvTaps)), ("fork", vp), ("row_stats", vp)]
 
 
 class AttnArgs(C.Structure):
@@ -89,6 +89,7 @@ _SIGS = {
     "lp_cond_row": ([vp, C.c_int, vp, vp, C.c_int, vp, vp, C.c_int, vp, vp, C.c_int, vp], C.c_int),
     "lp_add_row": ([vp, vp, vp, C.c_int, C.c_int, vp], C.c_int),
     "lp_norm_mod": ([vp, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp, vp, C.c_int, vp], C.c_int),
+    "lp_norm_mod_stats": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp, vp, C.c_int, vp], C.c_int),
     "lp_sink_refresh": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_float, vp,
                          C.POINTER(RopeGeom), vp, vp, C.c_int, C.c_int, i64, i64, vp, vp], C.c_int),
     "lp_sink_refresh_temporal": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.POINTER(RopeGeom), vp,

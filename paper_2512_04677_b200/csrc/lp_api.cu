@@ -29,6 +29,8 @@ int cond_row(const float*, int, const float*, const float*, int, const float*, c
              float*, int, cudaStream_t);
 int add_row(const float*, const float*, float*, int, int, cudaStream_t);
 int norm_mod(const float*, int, int, int, float, const float*, const float*, void*, int, cudaStream_t);
+int norm_mod_stats(const float*, const float*, int, int, int, float, const float*, const float*, void*, int,
+                   cudaStream_t);
 int sink_refresh(const float*, const float*, int, int, int, int, const float*, float, const lp_block_desc*,
                  const lp_rope_geom&, void*, void*, int, int, int64_t, int64_t, float*, cudaStream_t);
 int sink_refresh_temporal(const float*, const float*, int, int, int, int, const float*, const lp_block_desc*,
@@ -109,6 +111,7 @@ int lp_gemm(const lp_gemm_args* a, void* stream) {
   if (a->in_dtype == LP_BF16) return gemm_tc(a, S(stream));
   LP_CHECK_ARG(a->in_dtype == LP_F32, "lp_gemm: in_dtype must be LP_F32 or LP_BF16");
   if (a->conv) return fail(LP_EUNSUPPORTED, "lp_gemm: conv taps need bf16 operands");
+  if (a->row_stats) return fail(LP_EUNSUPPORTED, "lp_gemm: row_stats is a bf16 (tcgen05) RESID epilogue");
   if (a->epilogue == LP_EPI_QKV)
     return fail(LP_EUNSUPPORTED, "lp_gemm: fp32 QKV epilogue is lp_gemm(STORE) + lp_qkv_post");
   if (a->epilogue == LP_EPI_EULER)
@@ -156,6 +159,11 @@ int lp_add_row(const float* x, const float* c, float* h, int rows, int d, void* 
 int lp_norm_mod(const float* h, int rows, int d, int mode, float eps, const float* shift, const float* scale,
                 void* out, int out_dtype, void* stream) {
   return norm_mod(h, rows, d, mode, eps, shift, scale, out, out_dtype, S(stream));
+}
+
+int lp_norm_mod_stats(const float* h, const float* stats, int rows, int d, int mode, float eps, const float* shift,
+                      const float* scale, void* out, int out_dtype, void* stream) {
+  return norm_mod_stats(h, stats, rows, d, mode, eps, shift, scale, out, out_dtype, S(stream));
 }
 
 int lp_sink_refresh(const float* k_raw, const float* v_raw, int s_tokens, int d, int n_heads, int qk_norm,

@@ -90,6 +90,8 @@ struct AttnParams {
                   // rerun exactly; exact kernel: non-null = rerun only those
   int flag_pairs; // flags written per CTA of a cluster pair (2 per work unit)
   int unit_base;  // first unit of this launch (the ragged tail runs as its own launch)
+  int l2pol;      // persistent kernel L2 hints (A/B, LP_ATTN_L2POL): bit 0 = Q evict_first,
+                  // bit 1 = K/V evict_normal (default 0: everything evict_last)
 };
 
 // Unit u -> (head, pair): regular units (both Q tiles valid) first, head-major
@@ -1147,7 +1149,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
   if (warp == 0 || warp == 3) {
     // ------------------------------------------------ TMA producers (both CTAs)
     if (elect_one()) {
-      const uint64_t pol = l2_policy_evict_last();
+      const uint64_t pol = (p.l2pol & 2) ? l2_policy_evict_normal() : l2_policy_evict_last();
+      const uint64_t pol_q = (p.l2pol & 1) ? l2_policy_evict_first() : pol;
       uint32_t g = 0;  // global K (warp 0) or V (warp 3) tile counter
       int k = 0;       // item count of this cluster
       for (int it = c; it < n_items; it += G, ++k) {
@@ -1162,8 +1165,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
           uint8_t* sq = smem + Attn2pSmem::Q_OFF + qb * AT_TILE_BYTES;
           const int q0 = im.pair * (2 * AT_M) + (int)rank * AT_M;
           if (rank == 0) mbar_arrive_expect_tx(&q_full[qb], 2 * AT_TILE_BYTES);
-          tma_load_2d_2sm(sq, &tmQ, &q_full[qb], col0, q0, pol);
-          tma_load_2d_2sm(sq + AT_HALF, &tmQ, &q_full[qb], col0 + 64, q0, pol);
+          tma_load_2d_2sm(sq, &tmQ, &q_full[qb], col0, q0, pol_q);
+          tma_load_2d_2sm(sq + AT_HALF, &tmQ, &q_full[qb], col0 + 64, q0, pol_q);
           for (int t = 0; t < im.n_tiles; ++t, ++g, cur.next()) {
             const int ks = g % A2_KS;
             mbar_wait(&k_empty[ks], ((g / A2_KS) & 1) ^ 1);
@@ -1606,6 +1609,8 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
   p.desc = a->desc;
   p.part_o = static_cast<float*>(a->workspace);
   p.unit_base = 0;
+  static const int l2pol = getenv("LP_ATTN_L2POL") ? atoi(getenv("LP_ATTN_L2POL")) : 0;
+  p.l2pol = l2pol;
   const int smem = AttnSmem::TOTAL;
   if (pair_k) {
     const PairLayout lay = pair_layout(a->n_q, a->n_heads);

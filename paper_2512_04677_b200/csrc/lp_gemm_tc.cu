@@ -42,6 +42,7 @@ struct GemmParams {
   int conv_kpt;
   int tap_row[27];
   int conv_t, conv_h, conv_w;  // halo conv (conv_tc_kernel): interior frames, height, width
+  float2* stats;  // RESID: per-row (mean, M2) of each 32-column chunk of the new h, [m][n/32]
 };
 
 __device__ __forceinline__ void a_coords(const GemmParams& p, int kb, int m0, int& col, int& row) {
@@ -226,6 +227,22 @@ __device__ __forceinline__ void gemm_epilogue_tile(const GemmParams& p, int row,
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) __stcs(h + q, o[q]);
+        if (p.stats) {
+          // LayerNorm partials of the updated row chunk for the next norm pass
+          // (two-pass on the registers: exact mean, then the squared deviations)
+          float s4[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) s4[j] = (o[2 * j].x + o[2 * j].y) + (o[2 * j].z + o[2 * j].w) +
+                                              ((o[2 * j + 1].x + o[2 * j + 1].y) + (o[2 * j + 1].z + o[2 * j + 1].w));
+          const float mc = ((s4[0] + s4[1]) + (s4[2] + s4[3])) * (1.0f / 32.0f);
+          float q4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float a = o[q].x - mc, b = o[q].y - mc, e = o[q].z - mc, f = o[q].w - mc;
+            q4[q & 3] = fmaf(a, a, fmaf(b, b, fmaf(e, e, fmaf(f, f, q4[q & 3]))));
+          }
+          p.stats[(int64_t)row * (p.n / 32) + col / 32] = make_float2(mc, (q4[0] + q4[1]) + (q4[2] + q4[3]));
+        }
       } else {
         if (p.epilogue == LP_EPI_STORE && p.bias) {
 #pragma unroll
@@ -836,6 +853,12 @@ int gemm_tc(const lp_gemm_args* a, cudaStream_t st) {
   p.ldc = a->ldc;
   p.bias = a->bias;
   p.gate = a->gate;
+  p.stats = nullptr;
+  if (a->row_stats) {
+    LP_CHECK_ARG(a->epilogue == LP_EPI_RESID && a->n % 32 == 0 && !a->conv,
+                 "gemm_tc: row_stats needs a RESID epilogue with n % 32 == 0");
+    p.stats = reinterpret_cast<float2*>(a->row_stats);
+  }
   memset(&p.qkv, 0, sizeof(p.qkv));
   memset(&p.euler, 0, sizeof(p.euler));
   p.conv_kpt = 0;

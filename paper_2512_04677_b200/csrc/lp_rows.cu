@@ -143,6 +143,75 @@ __global__ void __launch_bounds__(THREADS) norm_mod_kernel(const float* __restri
   }
 }
 
+// LayerNorm(+AdaLN) apply pass whose row statistics were produced by the
+// RESID GEMM epilogue that wrote h (lp_gemm_args.row_stats): per row, d/32
+// partials (mean, M2) of 32-column chunks.  One warp per row (grid-stride):
+// the lanes merge the partials (Chan et al.: fixed order in-lane, then a
+// shfl_down tree into lane 0, broadcast), then stream the row -- no second
+// read of h for the variance, no block-wide barriers, 8 float4 loads in
+// flight per lane.  Same math as norm_mod_kernel up to the fp32 rounding of
+// the merged moments.
+__device__ __forceinline__ void chan_merge(float& n, float& m, float& q, float nb, float mb, float qb) {
+  const float nt = n + nb;
+  if (nb == 0.0f) return;
+  const float dl = mb - m, f = nb / nt;
+  m = fmaf(dl, f, m);
+  q = q + qb + dl * dl * n * f;
+  n = nt;
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(256) norm_apply_kernel(const float* __restrict__ h,
+                                                         const float2* __restrict__ stats, int rows, int d,
+                                                         int mode, float eps, const float* __restrict__ shift,
+                                                         const float* __restrict__ scale, OutT* __restrict__ out) {
+  const int lane = threadIdx.x % 32;
+  const int nwarps = gridDim.x * (blockDim.x / 32);
+  const int np = d / 32;  // partials per row
+  for (int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; row < rows; row += nwarps) {
+    const float2* st = stats + (int64_t)row * np;
+    float n = 0.0f, m = 0.0f, q = 0.0f;
+    for (int i = lane; i < np; i += 32) {
+      const float2 t = st[i];
+      chan_merge(n, m, q, 32.0f, t.x, t.y);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float nb = __shfl_down_sync(0xffffffffu, n, o);
+      const float mb = __shfl_down_sync(0xffffffffu, m, o);
+      const float qb = __shfl_down_sync(0xffffffffu, q, o);
+      if (lane < o) chan_merge(n, m, q, nb, mb, qb);
+    }
+    const float mu = __shfl_sync(0xffffffffu, m, 0);
+    const float rstd = rsqrtf(__shfl_sync(0xffffffffu, q, 0) / d + eps);
+    const float* x = h + (int64_t)row * d;
+    OutT* o = out + (int64_t)row * d;
+    for (int c0 = lane * 4; c0 < d; c0 += 32 * 4 * 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * 128;
+        if (c < d) v[u] = __ldcs(reinterpret_cast<const float4*>(x + c));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * 128;
+        if (c >= d) break;
+        float y[4] = {(v[u].x - mu) * rstd, (v[u].y - mu) * rstd, (v[u].z - mu) * rstd, (v[u].w - mu) * rstd};
+        if (mode == 2) {
+          const float4 sc = __ldg(reinterpret_cast<const float4*>(scale + c));
+          const float4 sh = __ldg(reinterpret_cast<const float4*>(shift + c));
+          y[0] = y[0] * (1.0f + sc.x) + sh.x;
+          y[1] = y[1] * (1.0f + sc.y) + sh.y;
+          y[2] = y[2] * (1.0f + sc.z) + sh.z;
+          y[3] = y[3] * (1.0f + sc.w) + sh.w;
+        }
+        store4<OutT>(o + c, y);
+      }
+    }
+  }
+}
+
 // ----------------------------------------------------------- sink refresh --
 // One warp per (sink token, head): optional RMSNorm(k) then rotation at the
 // sink position i + delta (kvcache.py:86-90, denoiser.py:249); v copied.
@@ -455,6 +524,131 @@ __global__ void history_noise_bf16x8_kernel(__nv_bfloat16* __restrict__ arena, i
   }
 }
 
+// Perf-run noise, round 2b: the x8 kernel above spends 6 XU-pipe ops per
+// Box-Muller pair (2 I2F, LG2, SQRT, SIN, COS; 16/clk/SM) and two fmix32
+// rounds per word, which caps it near 2.5 TB/s.  Here each 32-bit word
+// w = fmix32(c * m + k) (one round; m odd and k per stream, so c -> w is a
+// bijection within a stream) drives one pair:
+//   radius  u = 2 - float(1.[w >> 12]) in (0, 1]  (20 bits, mantissa trick, no I2F)
+//           r = sqrt(-2 ln u) = sqrt(-2 ln2 * lg2 u)  (LG2 + SQRT: the only XU ops)
+//   angle   theta = (f + 1/2) / 1024 * pi/2 from 10 bits, sin/cos by one packed
+//           degree-4 Horner in theta^2 on the FMA pipe (|err| < 3e-5),
+//           and the quadrant by two independent sign bits: (+-r cos, +-r sin)
+//           with theta uniform on [0, pi/2) is (r cos phi, r sin phi) with phi
+//           uniform on [0, 2 pi) (the four sign patterns are the reflections
+//           into the four quadrants), i.e. exact Box-Muller.
+// Grid-stride over 16-byte chunks, two chunks per iteration with both loads
+// issued before the RNG work (memory-level parallelism).
+__device__ __forceinline__ uint64_t f32x2p(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void unpack_f32x2p(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2p(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+__device__ __forceinline__ void bm_pair(uint32_t w, float& z0, float& z1) {
+  const float x = __uint_as_float(0x3F800000u | ((w >> 9) & 0x007FFFF8u));  // [1, 2), 20 random bits
+  const float u = 2.0f - x;                                                 // (0, 1]
+  float l2, r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(u));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-1.3862943611198906f * l2));
+  const float y = __uint_as_float(0x3F800000u | ((w << 13) & 0x007FE000u));  // [1, 2), 10 bits
+  const float th = fmaf(y, 1.5707963267948966f, -1.5707963267948966f * (1.0f - 1.0f / 2048.0f));
+  const float t = th * th;
+  // (sin(th)/th, cos(th)) as polynomials in t, packed
+  uint64_t q = f32x2p(2.7557319e-06f, 2.4801587e-05f);
+  q = ffma2p(q, f32x2p(t, t), f32x2p(-1.9841270e-04f, -1.3888889e-03f));
+  q = ffma2p(q, f32x2p(t, t), f32x2p(8.3333333e-03f, 4.1666667e-02f));
+  q = ffma2p(q, f32x2p(t, t), f32x2p(-1.6666667e-01f, -0.5f));
+  q = ffma2p(q, f32x2p(t, t), f32x2p(1.0f, 1.0f));
+  float sn, cs;
+  unpack_f32x2p(q, sn, cs);
+  sn *= th;
+  z0 = __uint_as_float(__float_as_uint(r * cs) ^ ((w << 21) & 0x80000000u));  // sign: bit 10
+  z1 = __uint_as_float(__float_as_uint(r * sn) ^ ((w << 20) & 0x80000000u));  // sign: bit 11
+}
+
+__device__ __forceinline__ void noise8_bm(uint32_t m, uint32_t k, uint32_t ctr, float* z) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) bm_pair(fmix32((ctr * 4u + (uint32_t)j) * m + k), z[2 * j], z[2 * j + 1]);
+}
+
+__device__ __forceinline__ uint4 add_noise8(uint4 raw, const float* z, float sigma) {
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 x = __bfloat1622float2(h[j]);
+    h[j] = __floats2bfloat162_rn(fmaf(z[2 * j], sigma, x.x), fmaf(z[2 * j + 1], sigma, x.y));
+  }
+  return raw;
+}
+
+__global__ void __launch_bounds__(256) history_noise_bm_kernel(__nv_bfloat16* __restrict__ arena, int d, int layer,
+                                                              int kv, const lp_block_desc* __restrict__ desc) {
+  // per-segment tables, once per CTA: chunk base (cumulative), source and
+  // destination element offsets, and the stream's multiplier / offset
+  // (splitmix64 finaliser of (key, layer, kv, entry))
+  __shared__ int s_base[LP_MAX_SEG];
+  __shared__ int64_t s_src[LP_MAX_SEG], s_dst[LP_MAX_SEG];
+  __shared__ uint32_t s_m[LP_MAX_SEG], s_k[LP_MAX_SEG];
+  __shared__ int s_total;
+  const int n_hist = desc->n_seg - 2;
+  if (n_hist <= 0) return;
+  const int cpr = d / 8;  // 16-byte chunks per row
+  if (threadIdx.x == 0) {
+    int base = 0;
+    for (int e = 0; e < n_hist; ++e) {
+      s_base[e] = base;
+      base += desc->seg_len[e + 1] * cpr;
+    }
+    s_total = base;
+  }
+  if (threadIdx.x < n_hist) {
+    const int e = threadIdx.x;
+    s_src[e] = (int64_t)desc->src_row[e + 1] * d;
+    s_dst[e] = (int64_t)desc->seg_row[e + 1] * d;
+    uint64_t z = desc->noise_key ^ ((((uint64_t)(layer * 2 + kv) << 8) | (uint64_t)e) * 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    s_m[e] = (uint32_t)z | 1u;
+    s_k[e] = (uint32_t)(z >> 32);
+  }
+  __syncthreads();
+  const float sigma = desc->sigma;
+  const int total = s_total;
+  const int stride = gridDim.x * blockDim.x;
+  // chunks only grow along the grid-stride walk, so each of the two lanes of
+  // work keeps its segment index and advances it (usually zero steps)
+  int e0 = 0, e1 = 0;
+  for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < total; c0 += 2 * stride) {
+    const int c1 = c0 + stride;
+    while (e0 + 1 < n_hist && c0 >= s_base[e0 + 1]) ++e0;
+    while (e1 + 1 < n_hist && c1 >= s_base[e1 + 1]) ++e1;
+    const int r0 = c0 - s_base[e0], r1 = c1 - s_base[e1];
+    const bool has1 = c1 < total;
+    // both loads unconditional (the second re-reads chunk 0 past the end) so
+    // they issue back to back ahead of the RNG work
+    const uint4 raw0 = *reinterpret_cast<const uint4*>(arena + s_src[e0] + (int64_t)r0 * 8);
+    const uint4 raw1 =
+        *reinterpret_cast<const uint4*>(arena + (has1 ? s_src[e1] + (int64_t)r1 * 8 : s_src[e0] + (int64_t)r0 * 8));
+    float z[8];
+    noise8_bm(s_m[e0], s_k[e0], (uint32_t)r0, z);
+    *reinterpret_cast<uint4*>(arena + s_dst[e0] + (int64_t)r0 * 8) = add_noise8(raw0, z, sigma);
+    if (has1) {
+      noise8_bm(s_m[e1], s_k[e1], (uint32_t)r1, z);
+      *reinterpret_cast<uint4*>(arena + s_dst[e1] + (int64_t)r1 * 8) = add_noise8(raw1, z, sigma);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- launch ---
 static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
@@ -479,6 +673,9 @@ int preload_rows() {
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_kernel<float>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_kernel<__nv_bfloat16>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_bf16x8_kernel));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_bm_kernel));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_apply_kernel<__nv_bfloat16>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_apply_kernel<float>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, randn_kernel<float>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, randn_kernel<__nv_bfloat16>));
   return LP_OK;
@@ -521,6 +718,25 @@ int norm_mod(const float* h, int rows, int d, int mode, float eps, const float* 
     norm_mod_kernel<float, 256><<<rows, 256, 0, st>>>(h, d, mode, eps, shift, scale, (float*)out);
   }
   return launch_status("norm_mod");
+}
+
+int norm_mod_stats(const float* h, const float* stats, int rows, int d, int mode, float eps, const float* shift,
+                   const float* scale, void* out, int out_dtype, cudaStream_t st) {
+  LP_CHECK_ARG(mode == 1 || mode == 2, "norm_mod_stats: mode must be 1 (LayerNorm) or 2 (AdaLN)");
+  LP_CHECK_ARG(d % 32 == 0, "norm_mod_stats: d must be a multiple of 32");
+  LP_CHECK_ARG(h && stats && out, "norm_mod_stats: null pointer");
+  LP_CHECK_ARG(mode != 2 || (shift && scale), "norm_mod_stats: modulation needs shift and scale");
+  if (rows == 0) return LP_OK;
+  // 8 rows per 256-thread CTA, up to 8 CTAs per SM resident (grid-stride beyond)
+  const int want = nblk(rows, 8), cap = 8 * num_sms();
+  const int grid = want < cap ? want : cap;
+  const float2* s2 = reinterpret_cast<const float2*>(stats);
+  if (out_dtype == LP_BF16)
+    norm_apply_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(h, s2, rows, d, mode, eps, shift, scale,
+                                                           (__nv_bfloat16*)out);
+  else
+    norm_apply_kernel<float><<<grid, 256, 0, st>>>(h, s2, rows, d, mode, eps, shift, scale, (float*)out);
+  return launch_status("norm_mod_stats");
 }
 
 int sink_refresh(const float* kraw, const float* vraw, int s_tok, int d, int n_heads, int qk_norm,
@@ -620,7 +836,14 @@ int history_noise(void* arena, int dtype, int d, const float* noise, int n_layer
   int64_t n = (int64_t)max_rows * d;
   if (n == 0) return LP_OK;
   if (!noise && dtype == LP_BF16 && d % 8 == 0 && n < (1ll << 31)) {
-    history_noise_bf16x8_kernel<<<nblk(n / 8, 256), 256, 0, st>>>((__nv_bfloat16*)arena, d, layer, kv, desc);
+    static const bool x8 = getenv("LP_HIST_X8") != nullptr;  // round-2 kernel, A/B
+    if (x8) {
+      history_noise_bf16x8_kernel<<<nblk(n / 8, 256), 256, 0, st>>>((__nv_bfloat16*)arena, d, layer, kv, desc);
+    } else {
+      // two 16-byte chunks per thread and iteration; at most 8 CTAs per SM resident
+      const int want = nblk(n / 16, 256), cap = 8 * num_sms();
+      history_noise_bm_kernel<<<want < cap ? want : cap, 256, 0, st>>>((__nv_bfloat16*)arena, d, layer, kv, desc);
+    }
     return launch_status("history_noise");
   }
   int blocks = nblk((n + 3) / 4, 256);

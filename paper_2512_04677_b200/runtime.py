@@ -20,6 +20,7 @@ sigma > 0 (kvcache.py:121-137; the ring itself is never modified).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 import time
 
@@ -241,6 +242,13 @@ class Forward:
         self.att = torch.zeros((N, d), dtype=dt, device=dev)
         self.act = torch.zeros((N, f), dtype=dt, device=dev)
         self.qkv = torch.zeros((N, 3 * d), dtype=fp, device=dev) if self.fp32 else None
+        # bf16 pre-LN profiles: the RESID GEMMs (O-proj, FFN-down) write the
+        # LayerNorm partials of the h rows they update, so every later norm is
+        # one streaming apply pass (lp_norm_mod_stats); layer 0's input comes
+        # from the embedding and keeps the full lp_norm_mod.  LP_NO_NORM_STATS=1: A/B.
+        self.stats_on = (not self.fp32 and prof.pre_ln and d % 32 == 0
+                         and os.environ.get("LP_NO_NORM_STATS") is None)
+        self.row_stats = torch.zeros((N, d // 32, 2), dtype=fp, device=dev) if self.stats_on else None
         self.vel = torch.zeros((N, prof.out_dim), dtype=fp, device=dev)
         self.tok = torch.zeros((N, prof.patch_dim), dtype=dt, device=dev) if prof.patched else None
         self.c = torch.zeros(d, dtype=fp, device=dev)
@@ -356,7 +364,8 @@ class Forward:
             self._copy_done.record(st)
 
     # ------------------------------------------------------------- ops ------
-    def _gemm(self, st, a, lda, m, k, w, ldw, n, c, ldc, epi, out_dtype=None, bias=0, gate=0, qkv=None):
+    def _gemm(self, st, a, lda, m, k, w, ldw, n, c, ldc, epi, out_dtype=None, bias=0, gate=0, qkv=None,
+              stats=0):
         args = L.GemmArgs()
         args.in_dtype = self.dw.ldt
         args.out_dtype = self.dw.ldt if out_dtype is None else out_dtype
@@ -367,9 +376,11 @@ class Forward:
         args.bias, args.gate = bias, gate
         args.qkv = C.pointer(qkv) if qkv is not None else None
         args.fork = self.fork
+        args.row_stats = stats
         L.call("lp_gemm", C.byref(args), st)
 
-    def _proj(self, st, a, m, k, w_t, n, c, ldc, epi, out_dtype=None, bias=0, gate=0, w_col0=0, qkv=None):
+    def _proj(self, st, a, m, k, w_t, n, c, ldc, epi, out_dtype=None, bias=0, gate=0, w_col0=0, qkv=None,
+              stats=0):
         """y = a . W for a weight stored in the precision's layout.  fp32:
         W (k, n_total) row-major; bf16: W^T (n_total, k).  ``w_col0`` picks
         output columns [w_col0, w_col0 + n)."""
@@ -380,7 +391,19 @@ class Forward:
         else:
             ldw = w_t.shape[-1]
             wp = w_t.data_ptr() + w_col0 * ldw * esz
-        self._gemm(st, a, k, m, k, wp, ldw, n, c, ldc, epi, out_dtype, bias, gate, qkv)
+        self._gemm(st, a, k, m, k, wp, ldw, n, c, ldc, epi, out_dtype, bias, gate, qkv, stats)
+
+    def _norm(self, st, mode, shift, scale, from_stats):
+        """xa = modulate(norm(h)): the full row-reduction kernel, or the apply
+        pass over the partials the last RESID GEMM left in row_stats."""
+        prof, ldt = self.prof, self.dw.ldt
+        N, d = self.n_tokens, prof.model_dim
+        if from_stats and self.stats_on and mode >= 1:
+            L.call("lp_norm_mod_stats", self.h.data_ptr(), self.row_stats.data_ptr(), N, d, mode, prof.eps,
+                   shift or None, scale or None, self.xa.data_ptr(), ldt, st)
+        else:
+            L.call("lp_norm_mod", self.h.data_ptr(), N, d, mode, prof.eps, shift or None, scale or None,
+                   self.xa.data_ptr(), ldt, st)
 
     # ---------------------------------------------------------- sink ---------
     def set_sink(self, sink_frame: torch.Tensor, stream=None) -> None:
@@ -486,8 +509,7 @@ class Forward:
             mp = (lambda k: mods.data_ptr() + k * d * 4) if prof.adaln else (lambda k: 0)
             # pre-attention norm / modulation
             self._tag("norm_mod", "begin", stream)
-            L.call("lp_norm_mod", self.h.data_ptr(), N, d, norm_mode, prof.eps, mp(0) or None, mp(1) or None,
-                   self.xa.data_ptr(), ldt, st)
+            self._norm(st, norm_mode, mp(0), mp(1), from_stats=l > 0)
             self._tag("norm_mod", "end", stream)
             epi = L.QkvEpi(d, prof.n_heads, prof.head_dim, int(prof.qk_norm), prof.eps,
                            _p(dw.g_q[l]) if prof.qk_norm else 0, _p(dw.g_k[l]) if prof.qk_norm else 0,
@@ -519,13 +541,13 @@ class Forward:
                 self.probe("attention", "end", stream)
             if self.probe:
                 self.probe("o_proj", "begin", stream)
+            stats = self.row_stats.data_ptr() if self.stats_on else 0
             self._proj(st, self.att.data_ptr(), N, d, dw.wo[l], d, self.h.data_ptr(), d, L.EPI_RESID,
-                       gate=mp(2))
+                       gate=mp(2), stats=stats)
             if self.probe:
                 self.probe("o_proj", "end", stream)
             self._tag("norm_mod", "begin", stream)
-            L.call("lp_norm_mod", self.h.data_ptr(), N, d, norm_mode, prof.eps, mp(3) or None, mp(4) or None,
-                   self.xa.data_ptr(), ldt, st)
+            self._norm(st, norm_mode, mp(3), mp(4), from_stats=True)
             self._tag("norm_mod", "end", stream)
             if self.probe:
                 self.probe("ffn_up", "begin", stream)
@@ -536,16 +558,14 @@ class Forward:
             if self.probe:
                 self.probe("ffn_down", "begin", stream)
             self._proj(st, self.act.data_ptr(), N, f, dw.w2[l], d, self.h.data_ptr(), d, L.EPI_RESID,
-                       gate=mp(5))
+                       gate=mp(5), stats=stats)
             if self.probe:
                 self.probe("ffn_down", "end", stream)
         # head + flow step (denoiser.py:268, latent.py:140-147)
         if prof.adaln:
-            L.call("lp_norm_mod", self.h.data_ptr(), N, d, 2, prof.eps, self.hmod.data_ptr(),
-                   self.hmod.data_ptr() + d * 4, self.xa.data_ptr(), ldt, st)
+            self._norm(st, 2, self.hmod.data_ptr(), self.hmod.data_ptr() + d * 4, from_stats=nl > 0)
         else:
-            L.call("lp_norm_mod", self.h.data_ptr(), N, d, 1 if prof.pre_ln else 0, prof.eps, None, None,
-                   self.xa.data_ptr(), ldt, st)
+            self._norm(st, 1 if prof.pre_ln else 0, 0, 0, from_stats=nl > 0)
         if self.fp32 or not self.fuse_euler:
             self._proj(st, self.xa.data_ptr(), N, d, dw.w_vel, prof.out_dim, self.vel.data_ptr(), prof.out_dim,
                        L.EPI_STORE, L.LP_F32)

@@ -20,7 +20,7 @@ def test_library_exports_every_header_symbol():
     assert len(syms) >= 20
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.lp_abi_version() == L.ABI_VERSION == 7
+    assert lib.lp_abi_version() == L.ABI_VERSION == 8
 
 
 def test_ctypes_signatures_cover_header():
@@ -31,10 +31,10 @@ def test_struct_layout_matches_c(tmp_path):
     src = tmp_path / "sz.c"
     src.write_text(
         '#include <stdio.h>\n#include <stddef.h>\n#include "livepipe_b200.h"\n'
-        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(lp_block_desc),"
+        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(lp_block_desc),"
         " sizeof(lp_rope_geom), sizeof(lp_qkv_epi), sizeof(lp_gemm_args), sizeof(lp_attn_args),"
         " offsetof(lp_block_desc, noise_key), offsetof(lp_gemm_args, qkv), sizeof(lp_conv_taps),"
-        " offsetof(lp_gemm_args, conv));return 0;}\n")
+        " offsetof(lp_gemm_args, conv), offsetof(lp_gemm_args, row_stats));return 0;}\n")
     exe = tmp_path / "sz"
     r = subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
                        capture_output=True, text=True)
@@ -43,7 +43,8 @@ def test_struct_layout_matches_c(tmp_path):
     got = [int(x) for x in subprocess.check_output([str(exe)]).split()]
     want = [ctypes.sizeof(L.BlockDesc), ctypes.sizeof(L.RopeGeom), ctypes.sizeof(L.QkvEpi),
             ctypes.sizeof(L.GemmArgs), ctypes.sizeof(L.AttnArgs), L.BlockDesc.noise_key.offset,
-            L.GemmArgs.qkv.offset, ctypes.sizeof(L.ConvTaps), L.GemmArgs.conv.offset]
+            L.GemmArgs.qkv.offset, ctypes.sizeof(L.ConvTaps), L.GemmArgs.conv.offset,
+            L.GemmArgs.row_stats.offset]
     assert got == want
 
 

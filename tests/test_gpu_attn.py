@@ -211,3 +211,35 @@ def test_device_history_noise_moments(dtype):
     assert abs(kurt - 3.0) < 0.1, kurt
     assert abs(float((z.abs() > 2.0).float().mean()) - 0.0455) < 0.003  # two-sided 2-sigma tail
     assert torch.all(arena[0:n_tok] == 1.0)  # stored ring untouched
+
+
+def test_device_history_noise_streams_independent():
+    # perf-run noise: every (layer, K/V, entry) stream and every (block, step)
+    # key draws its own N(0,1) sequence -- no two streams may repeat or
+    # correlate (the reference draws each corrupted view from its own Prng,
+    # engine.py:217-224 / kvcache.py:121-137)
+    d, n_tok, rows = 512, 256, 4096
+    sigma = 1.0
+    ldt = L.LP_BF16
+    outs = []
+    for key, layer, kv in [(7, 0, 0), (7, 0, 1), (7, 1, 0), (8, 0, 0)]:
+        arena = torch.zeros((rows, d), dtype=torch.bfloat16, device=DEV)
+        desc = make_desc(4, [(3000, 8), (1000, n_tok), (2000, n_tok), (3100, 8)], 3100, 8, 128)
+        desc.src_row[1] = 0
+        desc.src_row[2] = 0
+        desc.sigma = sigma
+        desc.noise_key = key
+        ddev = upload_desc(desc)
+        L.call("lp_history_noise", arena.data_ptr(), ldt, d, None, 2, layer, kv, ddev.data_ptr(), 2 * n_tok,
+               torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        outs.append(arena[1000:1000 + n_tok].float().flatten())
+        outs.append(arena[2000:2000 + n_tok].float().flatten())  # second history entry
+        assert torch.all(arena[0:n_tok] == 0)
+    for i in range(len(outs)):
+        z = outs[i]
+        assert abs(float(z.mean())) < 0.01 and abs(float(z.std()) - 1.0) < 0.02
+        for j in range(i):
+            c = float(torch.corrcoef(torch.stack([outs[i], outs[j]]))[0, 1])
+            assert abs(c) < 0.015, (i, j, c)
+            assert not torch.equal(outs[i], outs[j])

@@ -32,8 +32,9 @@ def _fork():
     return _FORK[0]
 
 
-def _gemm(a, w_t, c, epi, out_dtype, bias=None, gate=None, qkv=None, in_dtype=L.LP_BF16, fork=False):
+def _gemm(a, w_t, c, epi, out_dtype, bias=None, gate=None, qkv=None, in_dtype=L.LP_BF16, fork=False, stats=None):
     args = L.GemmArgs()
+    args.row_stats = stats.data_ptr() if stats is not None else None
     args.fork = _fork() if fork else None
     args.in_dtype, args.out_dtype, args.epilogue = in_dtype, out_dtype, epi
     args.m, args.k = a.shape
@@ -346,3 +347,43 @@ def test_ffn_up_gelu_at_benched_14b_shape():
     c = torch.zeros((m, n), device=DEV, dtype=torch.bfloat16)
     _gemm(a, w, c, L.EPI_GELU, L.LP_BF16, fork=True)
     assert rel_l2(c.float().cpu(), ref.cpu()) < 5e-3
+
+
+@pytest.mark.parametrize("m,k,n,fork", [(300, 256, 512, False), (4680, 5120, 5120, True), (4680, 13824, 5120, True)])
+def test_resid_row_stats_feed_the_norm_apply_pass(m, k, n, fork):
+    # AdaLN with its reduction fused into the producing RESID GEMM: the
+    # epilogue's (mean, M2) per 32-column chunk of the new h, merged by
+    # lp_norm_mod_stats, gives the same modulated norm as the full-row
+    # lp_norm_mod (K7: pre-LN + AdaLN of the Wan profile); 14B O-proj and
+    # FFN-down shapes run through the pair + side-stream tail split
+    a, w = _ab(m, k, n, 7)
+    g = torch.Generator(device=DEV).manual_seed(8)
+    h0 = torch.randn((m, n), generator=g, device=DEV) * 3.0 + 0.5
+    gate = torch.rand(n, generator=g, device=DEV) + 0.5
+    h = h0.clone()
+    stats = torch.full((m, n // 32, 2), float("nan"), device=DEV)
+    _gemm(a, w, h, L.EPI_RESID, L.LP_F32, gate=gate, fork=fork, stats=stats)
+    ref_h = h0 + gate * (a.float() @ w.float().T)
+    assert rel_l2(h.cpu(), ref_h.cpu()) < 1e-5
+    chunks = h.reshape(m, n // 32, 32)
+    torch.testing.assert_close(stats[..., 0], chunks.mean(-1), rtol=1e-5, atol=1e-5)
+    torch.testing.assert_close(stats[..., 1], ((chunks - chunks.mean(-1, keepdim=True)) ** 2).sum(-1),
+                               rtol=1e-4, atol=1e-4)
+    shift = torch.randn(n, generator=g, device=DEV) * 0.1
+    scale = torch.randn(n, generator=g, device=DEV) * 0.1
+    st = torch.cuda.current_stream().cuda_stream
+    for mode in (1, 2):
+        want = torch.empty((m, n), dtype=torch.bfloat16, device=DEV)
+        got = torch.empty_like(want)
+        sh, sc = (shift.data_ptr(), scale.data_ptr()) if mode == 2 else (None, None)
+        L.call("lp_norm_mod", h.data_ptr(), m, n, mode, 1e-6, sh, sc, want.data_ptr(), L.LP_BF16, st)
+        L.call("lp_norm_mod_stats", h.data_ptr(), stats.data_ptr(), m, n, mode, 1e-6, sh, sc, got.data_ptr(),
+               L.LP_BF16, st)
+        torch.cuda.synchronize()
+        ln = torch.nn.functional.layer_norm(h, (n,), eps=1e-6)
+        ref = ln * (1 + scale) + shift if mode == 2 else ln
+        assert rel_l2(got.float().cpu(), ref.cpu()) < 4e-3
+        # the two kernels differ only in fp32 rounding of the moments: at most one bf16 ulp apart
+        diff = (got.float() - want.float()).abs()
+        assert float((diff > 0).float().mean()) < 0.01
+        assert bool(torch.all(diff <= want.float().abs() * 2 ** -7 + 1e-6))
