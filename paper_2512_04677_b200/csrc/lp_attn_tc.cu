@@ -92,6 +92,8 @@ struct AttnParams {
   int unit_base;  // first unit of this launch (the ragged tail runs as its own launch)
   int l2pol;      // persistent kernel L2 hints (A/B, LP_ATTN_L2POL): bit 0 = Q evict_first,
                   // bit 1 = K/V evict_normal (default 0: everything evict_last)
+  int* sched;     // persistent kernel: global item counter (zeroed before the launch) for
+                  // dynamic item assignment, or NULL: static round robin
 };
 
 // Unit u -> (head, pair): regular units (both Q tiles valid) first, head-major
@@ -1057,6 +1059,10 @@ struct Attn2pSmem {
   static constexpr int TOTAL = SEG_OFF + 2 * LP_MAX_SEG * 4 + 16 + 1024;
 };
 
+// sched_empty arrivals per item: leader warps 1, 2, 3 + 8 softmax warps;
+// partner warps 0, 3 + 8 softmax warps
+constexpr int SCHED_CONSUMERS = 11 + 10;
+
 struct Item {  // one work unit or KV piece, as every role derives it
   int head, pair, piece, t_first, n_tiles;
 };
@@ -1099,6 +1105,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
   uint64_t* o_free = o_done + 1;         // leader: the epilogue read O (8 warps x 2 CTAs)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
   int* win_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  // dynamic item queue (p.sched): a 4-slot ring of item indices per CTA,
+  // filled by the leader's Q/K producer thread (one atomicAdd per item) and
+  // released by every consumer role of both CTAs on the leader's sched_empty
+  uint64_t* sched_full = reinterpret_cast<uint64_t*>(smem + Attn2pSmem::BAR_OFF + 384);  // [4] both
+  uint64_t* sched_empty = sched_full + 4;                                                  // [4] leader
+  int* sched_item = reinterpret_cast<int*>(sched_empty + 4);                               // [4] both
   float* xm = reinterpret_cast<float*>(smem + Attn2pSmem::XM_OFF);
   float* xl = reinterpret_cast<float*>(smem + Attn2pSmem::XL_OFF);
   int* seg_row = reinterpret_cast<int*>(smem + Attn2pSmem::SEG_OFF);
@@ -1135,6 +1147,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
     }
     mbar_init(o_done, 1);
     mbar_init(o_free, 16);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&sched_full[i], 1);
+      mbar_init(&sched_empty[i], SCHED_CONSUMERS);
+    }
     fence_barrier_init();
   }
   cluster_sync_all();
@@ -1144,6 +1160,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int nt_total = n_seg_s[1];
+  const bool dyn = p.sched != nullptr;
+  // the cluster's k-th item: static round robin, or from the queue (consumer
+  // side; `single` = a one-thread role, else the whole warp reads the slot)
+  auto take_item = [&](int k, bool single) -> int {
+    if (!dyn) {
+      const int it = c + k * G;
+      return it < n_items ? it : -1;
+    }
+    mbar_wait(&sched_full[k & 3], (k >> 2) & 1);
+    if (rank) fence_acquire_cluster();
+    const int it = *reinterpret_cast<volatile int*>(&sched_item[k & 3]);
+    if (it >= 0) {  // the slot is released (the final -1 slot is never reused)
+      if (!single) __syncwarp();
+      if (single || lane == 0) {
+        if (rank) mbar_arrive_remote(&sched_empty[k & 3], 0);
+        else mbar_arrive(&sched_empty[k & 3]);
+      }
+    }
+    return it;
+  };
+  // producer side (leader's Q/K thread): claim the next item, publish it to both CTAs
+  auto claim_item = [&](int k) -> int {
+    if (!dyn) return take_item(k, true);
+    if (k >= 4) mbar_wait(&sched_empty[k & 3], ((k >> 2) - 1) & 1);
+    int it = atomicAdd(p.sched, 1);
+    if (it >= n_items) it = -1;
+    sched_item[k & 3] = it;
+    st_shared_remote_s32(&sched_item[k & 3], 1, it);
+    mbar_arrive(&sched_full[k & 3]);
+    mbar_arrive_remote_release(&sched_full[k & 3], 1);
+    return it;
+  };
 
   if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(AT_REG_CTRL));
   if (warp == 0 || warp == 3) {
@@ -1152,8 +1200,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
       const uint64_t pol = (p.l2pol & 2) ? l2_policy_evict_normal() : l2_policy_evict_last();
       const uint64_t pol_q = (p.l2pol & 1) ? l2_policy_evict_first() : pol;
       uint32_t g = 0;  // global K (warp 0) or V (warp 3) tile counter
-      int k = 0;       // item count of this cluster
-      for (int it = c; it < n_items; it += G, ++k) {
+      for (int k = 0;; ++k) {  // k: item count of this cluster
+        const int it = (warp == 0 && rank == 0) ? claim_item(k) : take_item(k, true);
+        if (it < 0) break;
         const Item im = item_of(p, it, nt_total);
         const int col0 = im.head * AT_D;
         TileCursor cur;
@@ -1192,8 +1241,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
     constexpr uint32_t IDESC_S = idesc_bf16_f32(2 * AT_M, AT_N);
     constexpr uint32_t IDESC_O = idesc_bf16_f32(2 * AT_M, AT_D, false, true);
     uint32_t g = 0;
-    int k = 0;
-    for (int it = c; it < n_items; it += G, ++k) {
+    for (int k = 0;; ++k) {
+      const int it = take_item(k, false);
+      if (it < 0) break;
       const Item im = item_of(p, it, nt_total);
       if (warp == 1) {
         const int qb = k & 1;
@@ -1255,8 +1305,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
     const float sc = p.scale_log2;
     const uint64_t sc2 = f32x2(sc, sc);
     uint32_t g = 0;
-    int k = 0;
-    for (int it = c; it < n_items; it += G, ++k) {
+    for (int k = 0;; ++k) {
+      const int it = take_item(k, false);
+      if (it < 0) break;
       const Item im = item_of(p, it, nt_total);
       const int g0 = (int)g;
       float m_run = 0.0f, l_run = 0.0f;
@@ -1548,8 +1599,15 @@ static bool persistent_attention() {
   static const bool persist = getenv("LP_ATTN_NONPERSIST") == nullptr;
   return persist;
 }
+// Dynamic item assignment in the persistent kernel (LP_ATTN_DYN=1): every
+// cluster claims the next item from a global counter, so the split plan is
+// the greedy-list makespan rather than the round-robin one.
+static bool dynamic_attention() {
+  static const bool dyn = getenv("LP_ATTN_DYN") != nullptr;
+  return dyn && persistent_attention();
+}
 static AttnPlan plan_pair(int n_q, int n_heads) {
-  return plan_attention(n_q, n_heads, num_sms() / 2, 1.0, persistent_attention());
+  return plan_attention(n_q, n_heads, num_sms() / 2, 1.0, persistent_attention() && !dynamic_attention());
 }
 
 // The product path: the pair kernel over every unit; with LP_ATTN_TAIL_SPLIT
@@ -1558,6 +1616,7 @@ static AttnPlan plan_pair(int n_q, int n_heads) {
 struct PairLayout {
   AttnPlan main;      // regular units only
   int n_tail = 0;     // ragged units (one per head) or 0
+  int64_t sched = 0;  // workspace offset of the dynamic item counter
   int64_t flags_main = 0, flags_tail = 0, bytes = 0;  // workspace offsets / total
 };
 static PairLayout pair_layout(int n_q, int n_heads) {
@@ -1575,7 +1634,8 @@ static PairLayout pair_layout(int n_q, int n_heads) {
   L.n_tail = ragged ? n_heads : 0;
   L.flags_main = partial_bytes(L.main);
   L.flags_tail = L.flags_main + flag_bytes(2 * L.main.grid());
-  L.bytes = L.flags_tail + flag_bytes(L.n_tail);
+  L.sched = L.flags_tail + flag_bytes(L.n_tail);
+  L.bytes = L.sched + 256;  // dynamic item counter
   return L;
 }
 
@@ -1611,6 +1671,7 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
   p.unit_base = 0;
   static const int l2pol = getenv("LP_ATTN_L2POL") ? atoi(getenv("LP_ATTN_L2POL")) : 0;
   p.l2pol = l2pol;
+  p.sched = nullptr;
   const int smem = AttnSmem::TOTAL;
   if (pair_k) {
     const PairLayout lay = pair_layout(a->n_q, a->n_heads);
@@ -1645,6 +1706,11 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
           const int clusters = std::min(pm.grid(), std::max(1, num_sms() / 2));
           LP_CUDA_TRY(cudaFuncSetAttribute(attn_tc2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            Attn2pSmem::TOTAL));
+          q.sched = nullptr;
+          if (dynamic_attention()) {
+            q.sched = reinterpret_cast<int*>(ws + lay.sched);
+            LP_CUDA_TRY(cudaMemsetAsync(q.sched, 0, sizeof(int), st));
+          }
           attn_tc2p_kernel<<<2 * clusters, AT_THREADS, Attn2pSmem::TOTAL, st>>>(tq, tk2, tv, q, pm.grid());
           if ((rc = launch_status("attention_tc2p"))) return rc;
         } else {

@@ -195,16 +195,14 @@ __global__ void __launch_bounds__(128) attn_f32_kernel(const T* __restrict__ q, 
                                                        const T* __restrict__ varena, T* __restrict__ out, int n_q,
                                                        int n_heads, int hd, float scale,
                                                        const lp_block_desc* __restrict__ desc, int n_kv_max) {
-  extern __shared__ float logit[];  // [n_kv_max] logits, then the K tile and q
+  extern __shared__ float logit[];
   __shared__ float red[4];
   __shared__ float total_sum;
   const int tid = threadIdx.x, lane = tid % 32, wid = tid / 32;
   const int row = blockIdx.x / n_heads, head = blockIdx.x % n_heads;
   if (row >= n_q) return;
   const int d = n_heads * hd;
-  float* ktile = logit + n_kv_max;   // [128][hd + 1] (padded: conflict-free column reads)
-  float* qs = ktile + 128 * (hd + 1);
-  for (int c = tid; c < hd; c += blockDim.x) qs[c] = to_f32(q[(int64_t)row * d + head * hd + c]);
+  const T* qr = q + (int64_t)row * d + head * hd;
   // logits in reference key order: segments as listed in the descriptor
   int total = 0;
   for (int s = 0; s < desc->n_seg; ++s) total += desc->seg_len[s];
@@ -212,21 +210,11 @@ __global__ void __launch_bounds__(128) attn_f32_kernel(const T* __restrict__ q, 
   int base = 0;
   for (int s = 0; s < desc->n_seg; ++s) {
     const int r0 = desc->seg_row[s], len = desc->seg_len[s];
-    for (int j0 = 0; j0 < len; j0 += 128) {
-      // 128 keys staged with coalesced row reads, then one key per thread
-      __syncthreads();
-      for (int idx = tid; idx < 128 * hd; idx += blockDim.x) {
-        const int key = idx / hd, c = idx - key * hd;
-        ktile[key * (hd + 1) + c] =
-            j0 + key < len ? to_f32(karena[(int64_t)(r0 + j0 + key) * d + head * hd + c]) : 0.0f;
-      }
-      __syncthreads();
-      if (j0 + tid < len) {
-        const float* kr = ktile + tid * (hd + 1);
-        float acc = 0.0f;
-        for (int c = 0; c < hd; ++c) acc = __fadd_rn(acc, __fmul_rn(qs[c], kr[c]));
-        logit[base + j0 + tid] = __fmul_rn(acc, scale);
-      }
+    for (int j = tid; j < len; j += blockDim.x) {
+      const T* kr = karena + (int64_t)(r0 + j) * d + head * hd;
+      float acc = 0.0f;
+      for (int c = 0; c < hd; ++c) acc = __fadd_rn(acc, __fmul_rn(to_f32(qr[c]), to_f32(kr[c])));
+      logit[base + j] = __fmul_rn(acc, scale);
     }
     base += len;
   }
@@ -325,9 +313,8 @@ int qkv_post(const float* qkv, int m, const lp_qkv_epi& e, int out_dtype, cudaSt
 
 int attention_simt(const lp_attn_args* a, int n_kv_max, cudaStream_t st) {
   LP_CHECK_ARG(n_kv_max > 0, "attention: empty key set");
-  LP_CHECK_ARG(a->head_dim <= 128, "attention_simt: head_dim <= 128");
-  const size_t smem = ((size_t)n_kv_max + 128 * (a->head_dim + 1) + a->head_dim) * sizeof(float);
-  LP_CHECK_ARG(smem <= 220 * 1024, "attention_simt: too many keys for validation mode");
+  const size_t smem = (size_t)n_kv_max * sizeof(float);
+  LP_CHECK_ARG(smem <= 200 * 1024, "attention_simt: too many keys for validation mode");
   const int64_t blocks = (int64_t)a->n_q * a->n_heads;
   if (blocks == 0) return LP_OK;
   if (a->dtype == LP_BF16) {

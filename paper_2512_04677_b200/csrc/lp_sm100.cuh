@@ -245,6 +245,26 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
 // no cluster-scope fence (MEMBAR.GPU) per arrive.  For signals whose payload
 // is ordered by tcgen05 fences (a completed TMEM load / store), not by
 // generic-proxy memory.
+// Cluster-scope release of prior (local or st.shared::cluster) stores to the
+// CTA `cta` that waits on `bar` with mbar_wait + fence_acquire_cluster.
+__device__ __forceinline__ void mbar_arrive_remote_release(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+__device__ __forceinline__ void st_shared_remote_s32(int* p, uint32_t cta, int v) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "st.shared::cluster.s32 [ra], %2;\n\t}" ::"r"(smem_u32(p)),
+      "r"(cta), "r"(v)
+      : "memory");
+}
+__device__ __forceinline__ void fence_acquire_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
   asm volatile(
       "{\n\t.reg .b32 ra;\n\t"

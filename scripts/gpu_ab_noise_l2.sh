@@ -17,7 +17,7 @@ for pol in 1 3; do
   LP_ATTN_L2POL=$pol timeout 400 $B > $OUT/bench_l2pol$pol.json 2> $OUT/bench_l2pol$pol.err
 done
 for pol in 0 1 3; do
-  LP_ATTN_L2POL=$pol timeout 300 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct \
+  LP_ATTN_L2POL=$pol timeout 300 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct,lts__t_sectors_srcunit_tex.sum,lts__t_sectors_srcunit_tex_lookup_miss.sum,lts__t_sectors_srcunit_ltcfabric.sum,lts__t_requests_srcunit_ltcfabric_lookup_miss.sum \
     --clock-control none -k regex:attn_tc2p_kernel -s 300 -c 3 --csv \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-probe --no-decode > $OUT/ncu_l2pol$pol.csv 2> $OUT/ncu_l2pol$pol.err
 done
