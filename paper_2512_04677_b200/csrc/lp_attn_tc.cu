@@ -92,8 +92,20 @@ struct AttnParams {
   int unit_base;  // first unit of this launch (the ragged tail runs as its own launch)
   int l2pol;      // persistent kernel L2 hints (A/B, LP_ATTN_L2POL): bit 0 = Q evict_first,
                   // bit 1 = K/V evict_normal (default 0: everything evict_last)
-  int* sched;     // persistent kernel: global item counter (zeroed before the launch) for
+  int* sched;     // persistent kernel: global item counters (zeroed before the launch) for
                   // dynamic item assignment, or NULL: static round robin
+  // head-split queues (LP_ATTN_HEADSPLIT=T): clusters whose leader SM id is < T
+  // take the items of heads [0, H/2) first, the others heads [H/2, H); each
+  // queue is a list of item-index runs; an exhausted queue steals from the other
+  int hs_smid;       // T, or 0: one queue in item order.  sched[0..1]: queue counters,
+                     // sched[2..3]: items per queue, sched[4..5]: runs per queue,
+                     // sched[8 + 16 q + 2 r]: (first item, length) of run r of queue q
+};
+
+// Written into the workspace before each dynamic launch by sched_init_kernel
+// (by-value kernel argument, so a captured graph replays it unchanged).
+struct SchedTable {
+  int v[40];
 };
 
 // Unit u -> (head, pair): regular units (both Q tiles valid) first, head-major
@@ -1085,6 +1097,30 @@ __device__ __forceinline__ Item item_of(const AttnParams& p, int it, int nt_tota
   return r;
 }
 
+// Head-split queues: this SM's queue first, then steal from the other one
+// (out of line: it runs once per item on the leader's producer thread and
+// must not add to the 56-register control warps' pressure).
+__device__ __noinline__ int claim_head_split(int* sched, int smid_split) {
+  uint32_t smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  const int q0 = (int)smid < smid_split ? 0 : 1;
+  for (int t = 0; t < 2; ++t) {
+    const int q = t ? 1 - q0 : q0;
+    int j = atomicAdd(sched + q, 1);
+    if (j >= sched[2 + q]) continue;
+    const int* run = sched + 8 + 16 * q;
+    for (int r = 0; r < sched[4 + q]; ++r) {
+      if (j < run[2 * r + 1]) return run[2 * r] + j;
+      j -= run[2 * r + 1];
+    }
+  }
+  return -1;
+}
+
+__global__ void sched_init_kernel(int* sched, SchedTable t) {
+  if (threadIdx.x < 40) sched[threadIdx.x] = t.v[threadIdx.x];
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
     attn_tc2p_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const AttnParams p, int n_items) {
@@ -1184,8 +1220,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AT_THREADS, 1)
   auto claim_item = [&](int k) -> int {
     if (!dyn) return take_item(k, true);
     if (k >= 4) mbar_wait(&sched_empty[k & 3], ((k >> 2) - 1) & 1);
-    int it = atomicAdd(p.sched, 1);
-    if (it >= n_items) it = -1;
+    int it;
+    if (p.hs_smid > 0) {
+      it = claim_head_split(p.sched, p.hs_smid);
+    } else {
+      it = atomicAdd(p.sched, 1);
+      if (it >= n_items) it = -1;
+    }
     sched_item[k & 3] = it;
     st_shared_remote_s32(&sched_item[k & 3], 1, it);
     mbar_arrive(&sched_full[k & 3]);
@@ -1509,6 +1550,7 @@ int preload_attn_tc() {
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_tc2_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_tc2p_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, attn_combine_kernel));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, sched_init_kernel));
   return LP_OK;
 }
 
@@ -1606,6 +1648,31 @@ static bool dynamic_attention() {
   static const bool dyn = getenv("LP_ATTN_DYN") != nullptr;
   return dyn && persistent_attention();
 }
+// Head-split queues for the dynamic persistent kernel: the items of heads
+// [0, H/2) and [H/2, H) as runs of consecutive item indices (host mirror of
+// item_of / unit_coords).  False if a queue needs more than 8 runs.
+static bool head_split_queues(const AttnParams& q, int n_items, SchedTable& t) {
+  const int n_reg = q.reg_pairs * q.n_heads;
+  memset(&t, 0, sizeof(t));
+  for (int it = 0; it < n_items; ++it) {
+    const int unit = q.unit_base + (it < q.n_whole ? it : q.n_whole + (it - q.n_whole) / q.split);
+    const int head = unit < n_reg ? unit / q.reg_pairs : unit - n_reg;
+    const int g = head < q.n_heads / 2 ? 0 : 1;
+    int* run = t.v + 8 + 16 * g;
+    const int r = t.v[4 + g] - 1;
+    if (r >= 0 && run[2 * r] + run[2 * r + 1] == it) {
+      ++run[2 * r + 1];
+    } else {
+      if (r + 1 == 8) return false;
+      run[2 * (r + 1)] = it;
+      run[2 * (r + 1) + 1] = 1;
+      ++t.v[4 + g];
+    }
+    ++t.v[2 + g];
+  }
+  return true;
+}
+
 static AttnPlan plan_pair(int n_q, int n_heads) {
   return plan_attention(n_q, n_heads, num_sms() / 2, 1.0, persistent_attention() && !dynamic_attention());
 }
@@ -1672,6 +1739,7 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
   static const int l2pol = getenv("LP_ATTN_L2POL") ? atoi(getenv("LP_ATTN_L2POL")) : 0;
   p.l2pol = l2pol;
   p.sched = nullptr;
+  p.hs_smid = 0;
   const int smem = AttnSmem::TOTAL;
   if (pair_k) {
     const PairLayout lay = pair_layout(a->n_q, a->n_heads);
@@ -1709,7 +1777,16 @@ int attention_tc(const lp_attn_args* a, cudaStream_t st) {
           q.sched = nullptr;
           if (dynamic_attention()) {
             q.sched = reinterpret_cast<int*>(ws + lay.sched);
-            LP_CUDA_TRY(cudaMemsetAsync(q.sched, 0, sizeof(int), st));
+            static const int hs = getenv("LP_ATTN_HEADSPLIT") ? atoi(getenv("LP_ATTN_HEADSPLIT")) : 0;
+            SchedTable tab;
+            if (hs > 0 && head_split_queues(q, pm.grid(), tab)) {
+              q.hs_smid = hs;
+            } else {
+              memset(&tab, 0, sizeof(tab));
+              q.hs_smid = 0;
+            }
+            sched_init_kernel<<<1, 64, 0, st>>>(q.sched, tab);  // counters zeroed (+ the queue table)
+            if ((rc = launch_status("attention_sched_init"))) return rc;
           }
           attn_tc2p_kernel<<<2 * clusters, AT_THREADS, Attn2pSmem::TOTAL, st>>>(tq, tk2, tv, q, pm.grid());
           if ((rc = launch_status("attention_tc2p"))) return rc;
