@@ -46,6 +46,21 @@ def test_wan_rollout_matches_oracle(precision, tol):
     assert max(errs) < tol, errs
 
 
+def test_wan_rollout_with_epilogue_norm_stats_matches_oracle(monkeypatch):
+    # LP_NORM_STATS=1: LayerNorm statistics from the RESID GEMM epilogues +
+    # the apply pass (lp_norm_mod_stats) over a streamed bf16 rollout; TPP
+    # still bitwise equal to sequential
+    monkeypatch.setenv("LP_NORM_STATS", "1")
+    po, pp = _profiles(layers=3)
+    kw = dict(steps=4, blocks=5, cache_capacity=2)
+    ref = _oracle(po, **kw)
+    res = _engine(pp, "bf16", **kw)
+    errs = [rel_l2(b.values, r) for b, r in zip(res.blocks, ref)]
+    assert max(errs) < TOL_BF16, errs
+    tpp = _engine(pp, "bf16", mode="tpp", **kw)
+    assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(res.blocks, tpp.blocks))
+
+
 def test_wan_history_noise_fp32_matches_oracle():
     po, pp = _profiles(layers=1)
     kw = dict(steps=3, blocks=4, cache_capacity=2, history_sigma=0.2, history_mode="scaled")
