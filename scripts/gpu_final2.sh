@@ -17,5 +17,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-probe --no-decode > $OUT/ncu_launches.log 2>&1
 B="python bench.py --steps 1 --warmup 5 --no-cpu-baseline --no-probe --no-decode"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_tc2p_kernel -s 700 -c 1 -o $OUT/attn_p $B > $OUT/ncu_attn_p.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"norm_apply|history_noise_bm" -s 400 -c 2 -o $OUT/rows $B --history-sigma 0.1 > $OUT/ncu_rows.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:history_noise_bm -s 1000 -c 1 -o $OUT/hist $B --history-sigma 0.1 > $OUT/ncu_hist.log 2>&1
+LP_NORM_STATS=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"norm_apply|norm_mod" -s 700 -c 2 -o $OUT/norm $B > $OUT/ncu_norm.log 2>&1
+timeout 1200 python bench.py --long-horizon 834 --history-sigma 0.1 --no-cpu-baseline > $OUT/bench_long_horizon_834.json 2> $OUT/bench_long.err
 tail -8 $OUT/pytest_gpu.log; tail -2 $OUT/smoke.log; tail -c 400 $OUT/bench.json
