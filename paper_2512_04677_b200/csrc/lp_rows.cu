@@ -143,6 +143,73 @@ __global__ void __launch_bounds__(THREADS) norm_mod_kernel(const float* __restri
   }
 }
 
+// Software-pipelined form of norm_mod_kernel (modes 1/2, d <= 128 * 4 * NV):
+// a resident grid (a few CTAs per SM) walks the rows, and while a CTA
+// reduces and writes row r its loads of row r + G are already in flight
+// (two register buffers, ping-pong).  The one-row-per-CTA kernel runs its
+// waves in lock step -- every CTA of a wave loads, then reduces, then
+// writes -- so HBM idles during the reductions (3.6 TB/s at 14B).  Same
+// per-thread and block-reduction order as norm_mod_kernel: bitwise equal.
+template <typename OutT, int NV>
+__global__ void __launch_bounds__(128) norm_mod_pipe_kernel(const float* __restrict__ h, int rows, int d, int mode,
+                                                            float eps, const float* __restrict__ shift,
+                                                            const float* __restrict__ scale,
+                                                            OutT* __restrict__ out) {
+  constexpr int THREADS = 128;
+  __shared__ float red[32];
+  const int G = gridDim.x;
+  float4 a[NV], b[NV];
+  auto load = [&](float4(&v)[NV], int r) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * THREADS + threadIdx.x) * 4;
+      v[i] = (r < rows && c < d) ? __ldcs(reinterpret_cast<const float4*>(h + (int64_t)r * d + c))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto process = [&](const float4(&v)[NV], int r) {
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    const float mu = block_sum<THREADS>(s, red) / d;
+    float q = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * THREADS + threadIdx.x) * 4;
+      if (c < d) {
+        float x0 = v[i].x - mu, x1 = v[i].y - mu, x2 = v[i].z - mu, x3 = v[i].w - mu;
+        q += (x0 * x0 + x1 * x1) + (x2 * x2 + x3 * x3);
+      }
+    }
+    const float rstd = rsqrtf(block_sum<THREADS>(q, red) / d + eps);
+    OutT* o = out + (int64_t)r * d;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * THREADS + threadIdx.x) * 4;
+      if (c >= d) continue;
+      float y[4] = {(v[i].x - mu) * rstd, (v[i].y - mu) * rstd, (v[i].z - mu) * rstd, (v[i].w - mu) * rstd};
+      if (mode == 2) {
+        const float4 sc = __ldg(reinterpret_cast<const float4*>(scale + c));
+        const float4 sh = __ldg(reinterpret_cast<const float4*>(shift + c));
+        y[0] = y[0] * (1.0f + sc.x) + sh.x;
+        y[1] = y[1] * (1.0f + sc.y) + sh.y;
+        y[2] = y[2] * (1.0f + sc.z) + sh.z;
+        y[3] = y[3] * (1.0f + sc.w) + sh.w;
+      }
+      store4<OutT>(o + c, y);
+    }
+  };
+  int row = blockIdx.x;
+  load(a, row);
+  for (; row < rows; row += 2 * G) {
+    load(b, row + G);
+    process(a, row);
+    if (row + G >= rows) break;
+    load(a, row + 2 * G);
+    process(b, row + G);
+  }
+}
+
 // LayerNorm(+AdaLN) apply pass whose row statistics were produced by the
 // RESID GEMM epilogue that wrote h (lp_gemm_args.row_stats): per row, d/32
 // partials (mean, M2) of 32-column chunks.  One warp per row (grid-stride):
@@ -675,6 +742,10 @@ int preload_rows() {
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_bf16x8_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_bm_kernel));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_apply_kernel<__nv_bfloat16>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_pipe_kernel<__nv_bfloat16, 4>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_pipe_kernel<__nv_bfloat16, 10>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_pipe_kernel<float, 4>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_pipe_kernel<float, 10>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_apply_kernel<float>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, randn_kernel<float>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, randn_kernel<__nv_bfloat16>));
@@ -699,6 +770,25 @@ int norm_mod(const float* h, int rows, int d, int mode, float eps, const float* 
   LP_CHECK_ARG(mode == 0 || d % 4 == 0, "norm_mod: d must be a multiple of 4");
   LP_CHECK_ARG(mode != 2 || (shift && scale), "norm_mod: modulation needs shift and scale");
   if (rows == 0) return LP_OK;
+  static const bool pipe = getenv("LP_NORM_ONEROW") == nullptr;  // A/B: the one-row-per-CTA kernel
+  if (pipe && mode != 0 && d % 4 == 0 && d <= 128 * 4 * 10) {
+    // resident grid: 4 CTAs per SM (two row buffers per thread: ~100 registers)
+    const int cap = 4 * num_sms(), grid = rows < cap ? rows : cap;
+    if (d <= 2048) {
+      if (out_dtype == LP_BF16)
+        norm_mod_pipe_kernel<__nv_bfloat16, 4><<<grid, 128, 0, st>>>(h, rows, d, mode, eps, shift, scale,
+                                                                    (__nv_bfloat16*)out);
+      else
+        norm_mod_pipe_kernel<float, 4><<<grid, 128, 0, st>>>(h, rows, d, mode, eps, shift, scale, (float*)out);
+    } else {
+      if (out_dtype == LP_BF16)
+        norm_mod_pipe_kernel<__nv_bfloat16, 10><<<grid, 128, 0, st>>>(h, rows, d, mode, eps, shift, scale,
+                                                                     (__nv_bfloat16*)out);
+      else
+        norm_mod_pipe_kernel<float, 10><<<grid, 128, 0, st>>>(h, rows, d, mode, eps, shift, scale, (float*)out);
+    }
+    return launch_status("norm_mod");
+  }
   if (d <= 2048) {  // narrow rows (1.3B: d = 1536): 128 threads, 4 float4 per thread
     if (out_dtype == LP_BF16)
       norm_mod_kernel<__nv_bfloat16, 128, 4><<<rows, 128, 0, st>>>(h, d, mode, eps, shift, scale,

@@ -387,3 +387,25 @@ def test_resid_row_stats_feed_the_norm_apply_pass(m, k, n, fork):
         diff = (got.float() - want.float()).abs()
         assert float((diff > 0).float().mean()) < 0.01
         assert bool(torch.all(diff <= want.float().abs() * 2 ** -7 + 1e-6))
+
+
+@pytest.mark.parametrize("rows,d", [(1, 5120), (4680, 5120), (1001, 1536), (37, 2048), (300, 4096)])
+def test_norm_mod_matches_torch_layer_norm(rows, d):
+    # pre-LN + AdaLN (K7): the software-pipelined resident-grid kernel walks
+    # rows beyond the grid (4680 > 4 x 148) and handles partial float4 tails
+    g = torch.Generator(device=DEV).manual_seed(rows + d)
+    h = torch.randn((rows, d), generator=g, device=DEV) * 2.0 + 0.3
+    shift = torch.randn(d, generator=g, device=DEV) * 0.1
+    scale = torch.randn(d, generator=g, device=DEV) * 0.1
+    st = torch.cuda.current_stream().cuda_stream
+    ln = torch.nn.functional.layer_norm(h.double(), (d,), eps=1e-6)
+    for mode in (1, 2):
+        ref = (ln * (1 + scale.double()) + shift.double() if mode == 2 else ln).float()
+        out = torch.empty((rows, d), device=DEV)
+        sh, sc = (shift.data_ptr(), scale.data_ptr()) if mode == 2 else (None, None)
+        L.call("lp_norm_mod", h.data_ptr(), rows, d, mode, 1e-6, sh, sc, out.data_ptr(), L.LP_F32, st)
+        o16 = torch.empty((rows, d), device=DEV, dtype=torch.bfloat16)
+        L.call("lp_norm_mod", h.data_ptr(), rows, d, mode, 1e-6, sh, sc, o16.data_ptr(), L.LP_BF16, st)
+        torch.cuda.synchronize()
+        assert rel_l2(out.cpu(), ref.cpu()) < 1e-6
+        assert torch.equal(o16, out.to(torch.bfloat16))
