@@ -620,31 +620,13 @@ __device__ __forceinline__ uint64_t ffma2p(uint64_t a, uint64_t b, uint64_t c) {
   return r;
 }
 
-// Bit layout of a word: radius bits 0-19, angle bits 20-29, signs bits 30/31.
-// Shifts go through integer multiplies (IMAD / IMAD.HI on the FMA pipe) and
-// each mask-and-merge is one LOP3, so the 64-lane ALU pipe -- the limiter of
-// the first version (ncu: ALU 65 %, issue 73 %) -- carries ~half the ops.
-__device__ __forceinline__ uint32_t shr_fma(uint32_t x, int s) {  // x >> s as IMAD.HI
-  uint32_t r;
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(1u << (32 - s)));
-  return r;
-}
-__device__ __forceinline__ uint32_t fmix32_fma(uint32_t h) {
-  h ^= shr_fma(h, 16);
-  h *= 0x85EBCA6Bu;
-  h ^= shr_fma(h, 13);
-  h *= 0xC2B2AE35u;
-  h ^= shr_fma(h, 16);
-  return h;
-}
-
 __device__ __forceinline__ void bm_pair(uint32_t w, float& z0, float& z1) {
-  const float x = __uint_as_float(0x3F800000u | ((w * 8u) & 0x007FFFF8u));  // [1, 2), 20 random bits
+  const float x = __uint_as_float(0x3F800000u | ((w >> 9) & 0x007FFFF8u));  // [1, 2), 20 random bits
   const float u = 2.0f - x;                                                 // (0, 1]
   float l2, r;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(u));
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-1.3862943611198906f * l2));
-  const float y = __uint_as_float(0x3F800000u | (shr_fma(w, 7) & 0x007FE000u));  // [1, 2), 10 bits
+  const float y = __uint_as_float(0x3F800000u | ((w << 13) & 0x007FE000u));  // [1, 2), 10 bits
   const float th = fmaf(y, 1.5707963267948966f, -1.5707963267948966f * (1.0f - 1.0f / 2048.0f));
   const float t = th * th;
   // (sin(th)/th, cos(th)) as polynomials in t, packed
@@ -656,13 +638,13 @@ __device__ __forceinline__ void bm_pair(uint32_t w, float& z0, float& z1) {
   float sn, cs;
   unpack_f32x2p(q, sn, cs);
   sn *= th;
-  z0 = __uint_as_float(__float_as_uint(r * cs) ^ (w & 0x80000000u));         // sign: bit 31
-  z1 = __uint_as_float(__float_as_uint(r * sn) ^ ((w * 2u) & 0x80000000u));  // sign: bit 30
+  z0 = __uint_as_float(__float_as_uint(r * cs) ^ ((w << 21) & 0x80000000u));  // sign: bit 10
+  z1 = __uint_as_float(__float_as_uint(r * sn) ^ ((w << 20) & 0x80000000u));  // sign: bit 11
 }
 
 __device__ __forceinline__ void noise8_bm(uint32_t m, uint32_t k, uint32_t ctr, float* z) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) bm_pair(fmix32_fma((ctr * 4u + (uint32_t)j) * m + k), z[2 * j], z[2 * j + 1]);
+  for (int j = 0; j < 4; ++j) bm_pair(fmix32((ctr * 4u + (uint32_t)j) * m + k), z[2 * j], z[2 * j + 1]);
 }
 
 __device__ __forceinline__ uint4 add_noise8(uint4 raw, const float* z, float sigma) {
