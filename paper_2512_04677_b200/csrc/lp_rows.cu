@@ -693,39 +693,23 @@ __global__ void __launch_bounds__(256) history_noise_bm_kernel(__nv_bfloat16* __
   const int total = s_total;
   const int stride = gridDim.x * blockDim.x;
   // chunks only grow along the grid-stride walk, so each of the two lanes of
-  // work keeps its segment index and advances it (usually zero steps).  The
-  // loads of the next iteration are issued before this iteration's RNG work
-  // (software prefetch into registers): with the load next to its use, a
-  // thread had at most two 16-byte loads in flight and the kernel sat at
-  // ~2.7 TB/s, short of the concurrency HBM needs.
+  // work keeps its segment index and advances it (usually zero steps)
   int e0 = 0, e1 = 0;
-  auto src_of = [&](int c, int& e) -> const uint4* {
-    while (e + 1 < n_hist && c >= s_base[e + 1]) ++e;
-    return reinterpret_cast<const uint4*>(arena + s_src[e] + (int64_t)(c - s_base[e]) * 8);
-  };
-  int c0 = blockIdx.x * blockDim.x + threadIdx.x;
-  uint4 nx0 = make_uint4(0, 0, 0, 0), nx1 = nx0;
-  if (c0 < total) {
-    int ea = e0, eb = e1;
-    nx0 = *src_of(c0, ea);
-    nx1 = *src_of(c0 + stride < total ? c0 + stride : c0, eb);
-  }
-  for (; c0 < total; c0 += 2 * stride) {
+  for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < total; c0 += 2 * stride) {
     const int c1 = c0 + stride;
-    const uint4 raw0 = nx0, raw1 = nx1;
-    const int cn = c0 + 2 * stride;
-    if (cn < total) {  // prefetch the next iteration's chunks
-      int ea = e0, eb = e1;
-      nx0 = *src_of(cn, ea);
-      nx1 = *src_of(cn + stride < total ? cn + stride : cn, eb);
-    }
     while (e0 + 1 < n_hist && c0 >= s_base[e0 + 1]) ++e0;
     while (e1 + 1 < n_hist && c1 >= s_base[e1 + 1]) ++e1;
     const int r0 = c0 - s_base[e0], r1 = c1 - s_base[e1];
+    const bool has1 = c1 < total;
+    // both loads unconditional (the second re-reads chunk 0 past the end) so
+    // they issue back to back ahead of the RNG work
+    const uint4 raw0 = *reinterpret_cast<const uint4*>(arena + s_src[e0] + (int64_t)r0 * 8);
+    const uint4 raw1 =
+        *reinterpret_cast<const uint4*>(arena + (has1 ? s_src[e1] + (int64_t)r1 * 8 : s_src[e0] + (int64_t)r0 * 8));
     float z[8];
     noise8_bm(s_m[e0], s_k[e0], (uint32_t)r0, z);
     *reinterpret_cast<uint4*>(arena + s_dst[e0] + (int64_t)r0 * 8) = add_noise8(raw0, z, sigma);
-    if (c1 < total) {
+    if (has1) {
       noise8_bm(s_m[e1], s_k[e1], (uint32_t)r1, z);
       *reinterpret_cast<uint4*>(arena + s_dst[e1] + (int64_t)r1 * 8) = add_noise8(raw1, z, sigma);
     }

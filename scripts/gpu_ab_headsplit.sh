@@ -6,14 +6,6 @@ mkdir -p $OUT
 python -c "import torch; torch.zeros(1).cuda()" > /dev/null 2>&1
 LP_ATTN_DYN=1 LP_ATTN_HEADSPLIT=74 timeout 300 python -m pytest tests/test_gpu_attn.py -q --timeout 200 -rf > $OUT/pytest_attn_hs.log 2>&1
 echo "pytest rc=$?" >> $OUT/pytest_attn_hs.log
-timeout 300 python -m pytest tests/test_gpu_gemm.py -q -k "norm or row_stats" --timeout 200 -rf > $OUT/pytest_norm.log 2>&1
-echo "pytest rc=$?" >> $OUT/pytest_norm.log
-timeout 400 python bench.py --no-cpu-baseline --no-decode --steps 5 --warmup 3 > $OUT/bench_normpipe.json 2> $OUT/bench_normpipe.err
-LP_NORM_ONEROW=1 timeout 400 python bench.py --no-cpu-baseline --no-decode --steps 5 --warmup 3 > $OUT/bench_normonerow.json 2> $OUT/bench_normonerow.err
-timeout 300 python -m pytest tests/test_gpu_attn.py -q -k "noise" --timeout 200 -rf >> $OUT/pytest_norm.log 2>&1
-echo "pytest rc=$?" >> $OUT/pytest_norm.log
-timeout 400 python bench.py --no-cpu-baseline --no-decode --steps 5 --warmup 3 --history-sigma 0.1 > $OUT/bench_sigma_pf.json 2> $OUT/bench_sigma_pf.err
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:history_noise_bm -s 1000 -c 1 -o $OUT/hist   python bench.py --steps 1 --warmup 5 --no-cpu-baseline --no-probe --no-decode --history-sigma 0.1 > $OUT/ncu_hist.log 2>&1
 M=dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct,lts__t_sectors_srcunit_tex.sum,lts__t_sectors_srcunit_tex_lookup_miss.sum,lts__t_sectors_srcunit_ltcfabric.sum
 for v in static dyn 70 74 78; do
   unset LP_ATTN_DYN LP_ATTN_HEADSPLIT
@@ -23,4 +15,4 @@ for v in static dyn 70 74 78; do
     python bench.py --steps 1 --warmup 5 --no-cpu-baseline --no-probe --no-decode > $OUT/ncu_$v.csv 2> $OUT/ncu_$v.err
   timeout 400 python bench.py --no-cpu-baseline --no-decode --steps 5 --warmup 3 > $OUT/bench_$v.json 2> $OUT/bench_$v.err
 done
-tail -3 $OUT/pytest_attn_hs.log $OUT/pytest_norm.log
+tail -3 $OUT/pytest_attn_hs.log
