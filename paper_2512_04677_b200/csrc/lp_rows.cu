@@ -770,7 +770,9 @@ int norm_mod(const float* h, int rows, int d, int mode, float eps, const float* 
   LP_CHECK_ARG(mode == 0 || d % 4 == 0, "norm_mod: d must be a multiple of 4");
   LP_CHECK_ARG(mode != 2 || (shift && scale), "norm_mod: modulation needs shift and scale");
   if (rows == 0) return LP_OK;
-  static const bool pipe = getenv("LP_NORM_ONEROW") == nullptr;  // A/B: the one-row-per-CTA kernel
+  // LP_NORM_PIPE=1: the resident-grid pipelined kernel (measured slower: 43.6 vs 39.1 us at 14B,
+  // profiles/r2b/hs1_summary.md), kept for A/B
+  static const bool pipe = getenv("LP_NORM_PIPE") != nullptr;
   if (pipe && mode != 0 && d % 4 == 0 && d <= 128 * 4 * 10) {
     // resident grid: 4 CTAs per SM (two row buffers per thread: ~100 registers)
     const int cap = 4 * num_sms(), grid = rows < cap ? rows : cap;
