@@ -675,8 +675,12 @@ class Forward:
         if prof.adaln:
             n += 4
         # with a workspace the attention is the bounded-exponent kernel + the
-        # exact rerun of flagged units (+ the combine of the KV-split tail)
+        # exact rerun of flagged units (+ the combine of the KV-split tail),
+        # and the persistent kernel's dynamic item queue adds its init kernel
         per_layer = 7 + (1 if self.fp32 else 0) + (2 if self._sigma_on else 0) + (2 if self.attn_ws_bytes else 0)
+        if self.attn_ws_bytes and not self.fp32 and not any(
+                os.environ.get(k) for k in ("LP_ATTN_STATIC", "LP_ATTN_NONPERSIST", "LP_ATTN_SINGLE", "LP_ATTN_EXACT")):
+            per_layer += 1
         return n + prof.n_layers * per_layer + (3 if (self.fp32 or not self.fuse_euler) else 2)
 
     def velocity_host(self) -> np.ndarray:
