@@ -357,6 +357,15 @@ LP_API int lp_oracle_step(const float* x, const float* target, float s, float dt
 LP_API int lp_history_noise(void* arena, int dtype, int d, const float* noise, int n_layers, int layer,
                      int kv, const lp_block_desc* desc, int max_rows, void* stream);
 
+/* lp_history_noise (device counter-hash stream, bf16 arena) shaped to run on
+   a side stream beside the tcgen05 GEMMs: two 128-thread CTAs per SM of
+   <= 40 registers fit in what a GEMM CTA leaves free, so the corrupted-view
+   copy of layer l overlaps the previous layer's O-proj / FFN and this
+   layer's QKV instead of sitting on the critical path.  Same noise values
+   as lp_history_noise with noise == NULL.                                  */
+LP_API int lp_history_noise_co(void* arena, int d, int layer, int kv, const lp_block_desc* desc, int max_rows,
+                               void* stream);
+
 /* Device N(0,1) fp32 fill (perf-run weights / block noise), Philox4x32 +
    Box-Muller keyed by (seed, stream).  scale multiplies every sample.     */
 LP_API int lp_randn(float* out, int64_t n, uint64_t seed, uint64_t stream_id, float scale,

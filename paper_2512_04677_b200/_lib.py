@@ -110,6 +110,7 @@ _SIGS = {
                               C.c_int),
     "lp_codec_patch_encode": ([vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp], C.c_int),
     "lp_history_noise": ([vp, C.c_int, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
+    "lp_history_noise_co": ([vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
     "lp_randn": ([vp, i64, u64, u64, C.c_float, vp], C.c_int),
     "lp_randn_bf16": ([vp, i64, u64, u64, C.c_float, vp], C.c_int),
     "lp_link_send": ([vp, vp, i64, vp, vp, u32, C.c_int, vp, u64, vp, vp], C.c_int),

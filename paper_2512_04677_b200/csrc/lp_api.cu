@@ -40,6 +40,7 @@ int patchify(const float*, int, int, int, int, int, int, void*, int, cudaStream_
 int unpatchify_euler(const float*, const float*, int, int, int, int, int, int, const lp_block_desc*, float*,
                      cudaStream_t);
 int history_noise(void*, int, int, const float*, int, int, int, const lp_block_desc*, int, cudaStream_t);
+int history_noise_co(void*, int, int, int, const lp_block_desc*, int, cudaStream_t);
 int oracle_step(const float*, const float*, float, float, float*, float*, int64_t, cudaStream_t);
 int randn(void*, int64_t, uint64_t, uint64_t, float, int, cudaStream_t);
 int link_send(const void*, void*, int64_t, volatile uint32_t*, const volatile uint32_t*, uint32_t, int,
@@ -207,6 +208,11 @@ int lp_oracle_step(const float* x, const float* target, float s, float dt, float
 int lp_history_noise(void* arena, int dtype, int d, const float* noise, int n_layers, int layer, int kv,
                      const lp_block_desc* desc, int max_rows, void* stream) {
   return history_noise(arena, dtype, d, noise, n_layers, layer, kv, desc, max_rows, S(stream));
+}
+
+int lp_history_noise_co(void* arena, int d, int layer, int kv, const lp_block_desc* desc, int max_rows,
+                        void* stream) {
+  return history_noise_co(arena, d, layer, kv, desc, max_rows, S(stream));
 }
 
 int lp_randn(float* out, int64_t n, uint64_t seed, uint64_t stream_id, float scale, void* stream) {

@@ -657,8 +657,12 @@ __device__ __forceinline__ uint4 add_noise8(uint4 raw, const float* z, float sig
   return raw;
 }
 
-__global__ void __launch_bounds__(256) history_noise_bm_kernel(__nv_bfloat16* __restrict__ arena, int d, int layer,
-                                                              int kv, const lp_block_desc* __restrict__ desc) {
+// THREADS / MINB: 256 / 5 standalone (<= 48 registers); 128 / 12 for the co-resident form
+// (<= 40 registers: two CTAs fit beside a tcgen05 GEMM CTA's 168 x 320).
+template <int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) history_noise_bm_kernel(__nv_bfloat16* __restrict__ arena, int d,
+                                                                         int layer, int kv,
+                                                                         const lp_block_desc* __restrict__ desc) {
   // per-segment tables, once per CTA: chunk base (cumulative), source and
   // destination element offsets, and the stream's multiplier / offset
   // (splitmix64 finaliser of (key, layer, kv, entry))
@@ -740,7 +744,8 @@ int preload_rows() {
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_kernel<float>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_kernel<__nv_bfloat16>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_bf16x8_kernel));
-  LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_bm_kernel));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_bm_kernel<256, 5>));
+  LP_CUDA_TRY(cudaFuncGetAttributes(&a, history_noise_bm_kernel<128, 12>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_apply_kernel<__nv_bfloat16>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_pipe_kernel<__nv_bfloat16, 4>));
   LP_CUDA_TRY(cudaFuncGetAttributes(&a, norm_mod_pipe_kernel<__nv_bfloat16, 10>));
@@ -934,7 +939,8 @@ int history_noise(void* arena, int dtype, int d, const float* noise, int n_layer
     } else {
       // two 16-byte chunks per thread and iteration; at most 8 CTAs per SM resident
       const int want = nblk(n / 16, 256), cap = 8 * num_sms();
-      history_noise_bm_kernel<<<want < cap ? want : cap, 256, 0, st>>>((__nv_bfloat16*)arena, d, layer, kv, desc);
+      history_noise_bm_kernel<256, 5><<<want < cap ? want : cap, 256, 0, st>>>((__nv_bfloat16*)arena, d, layer, kv,
+                                                                              desc);
     }
     return launch_status("history_noise");
   }
@@ -945,6 +951,20 @@ int history_noise(void* arena, int dtype, int d, const float* noise, int n_layer
   else
     history_noise_kernel<float><<<blocks, 256, 0, st>>>((float*)arena, d, noise, n_layers, layer, kv, desc);
   return launch_status("history_noise");
+}
+
+// Co-resident form for a side stream beside the tensor-bound GEMMs: two
+// 128-thread CTAs per SM (the registers and shared memory a tcgen05 GEMM CTA
+// leaves free), grid-stride over the whole history.
+int history_noise_co(void* arena, int d, int layer, int kv, const lp_block_desc* desc, int max_rows, cudaStream_t st) {
+  LP_CHECK_ARG(d % 8 == 0, "history_noise_co: d must be a multiple of 8");
+  const int64_t n = (int64_t)max_rows * d;
+  if (n == 0) return LP_OK;
+  LP_CHECK_ARG(n < (1ll << 31), "history_noise_co: history too large");
+  const int want = nblk(n / 16, 128), cap = 2 * num_sms();
+  history_noise_bm_kernel<128, 12><<<want < cap ? want : cap, 128, 0, st>>>((__nv_bfloat16*)arena, d, layer, kv,
+                                                                              desc);
+  return launch_status("history_noise_co");
 }
 
 int randn(void* out, int64_t n, uint64_t seed, uint64_t stream, float scale, int dtype, cudaStream_t st) {

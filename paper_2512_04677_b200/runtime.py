@@ -504,6 +504,25 @@ class Forward:
         self._tag("sink_refresh", "end", stream)
         esz = ar.k.element_size()
         norm_mode = 2 if prof.adaln else (1 if prof.pre_ln else 0)
+        # device-RNG history noise on the side stream: layer l's copy is forked
+        # after attention(l-1) (layer 0: here) and joined before attention(l)
+        ov = self._sigma_on and self.noise is None and self._hist_side is not None
+        if ov:
+            main = stream if stream is not None else torch.cuda.current_stream(self.device)
+            side = self._hist_side
+            hist_rows = self.hist_rows or ar.hist_max * N
+
+            def noise_layer(l):
+                self._hist_fork[l].record(main)
+                side.wait_event(self._hist_fork[l])
+                for kv, arena_t in ((0, ar.k), (1, ar.v)):
+                    base = arena_t.data_ptr() + l * ar.layer_stride * esz
+                    self._tag("history_noise", "begin", side)
+                    L.call("lp_history_noise_co", base, d, l, kv, self.desc_ptr, hist_rows, side.cuda_stream)
+                    self._tag("history_noise", "end", side)
+                self._hist_join[l].record(side)
+
+            noise_layer(0)
         for l in range(nl):
             kl = ar.k.data_ptr() + l * ar.layer_stride * esz
             vl = ar.v.data_ptr() + l * ar.layer_stride * esz
@@ -527,7 +546,9 @@ class Forward:
                 if self.probe:
                     self.probe("qkv", "end", stream)
             # history noise into the scratch rows (corrupted view)
-            if self._sigma_on:
+            if ov:
+                main.wait_event(self._hist_join[l])
+            elif self._sigma_on:
                 for kv, base in ((0, kl), (1, vl)):
                     self._tag("history_noise", "begin", stream)
                     L.call("lp_history_noise", base, ldt, d, _p(self.noise), nl, l, kv, self.desc_ptr,
@@ -541,6 +562,8 @@ class Forward:
             L.call("lp_attention", C.byref(args), st)
             if self.probe:
                 self.probe("attention", "end", stream)
+            if ov and l + 1 < nl:
+                noise_layer(l + 1)  # its scratch rows were last read by this forward's predecessor
             if self.probe:
                 self.probe("o_proj", "begin", stream)
             stats = self.row_stats.data_ptr() if self.stats_on else 0
@@ -654,10 +677,22 @@ class Forward:
         hist = min(max(ar.n_slots - 1, ar.hist_max), L.MAX_SEG - 2)
         return ar.s_tokens + (hist + 1) * self.n_tokens
 
+    _hist_side = None
+
     def set_history_noise(self, on: bool, noise: torch.Tensor | None = None) -> None:
-        """Enable the corrupted-view path (graph topology changes with it)."""
+        """Enable the corrupted-view path (graph topology changes with it).
+        bf16 device-noise runs put the per-layer noise copies on a low-priority
+        side stream (lp_history_noise_co) that overlaps them with the previous
+        layer's O-proj / FFN and this layer's QKV; the stream and its events
+        are created here, at setup, never while a TPP link kernel may spin.
+        LP_HIST_OVERLAP=0 keeps them in line."""
         self._sigma_on = bool(on)
         self.noise = noise
+        if on and not self.fp32 and self._hist_side is None and os.environ.get("LP_HIST_OVERLAP", "1") != "0":
+            nl = self.prof.n_layers
+            self._hist_side = torch.cuda.Stream(self.device, priority=0)
+            self._hist_fork = [torch.cuda.Event() for _ in range(nl)]
+            self._hist_join = [torch.cuda.Event() for _ in range(nl)]
 
     graph_kernels = None  # kernel nodes of the captured forward graph (exact, set on capture)
 

@@ -298,6 +298,24 @@ def test_wan_tpp_long_stream_device_noise_equals_sequential(capacity):
     assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(seq.blocks, tpp.blocks))
 
 
+def test_history_noise_side_stream_equals_in_line(monkeypatch):
+    # device-RNG history noise on the low-priority side stream (lp_history_noise_co,
+    # forked after attention(l-1), joined before attention(l)) produces the
+    # same corrupted views as the in-line kernel: bitwise equal rollouts
+    _, pp = _profiles()
+    kw = dict(profile=pp, precision="bf16", steps=4, cache_capacity=3, blocks=8, device_inputs=True,
+              history_sigma=0.1, history_mode="fixed")
+    monkeypatch.setenv("LP_HIST_OVERLAP", "0")
+    inline = lp.run(lp.EngineConfig(mode="sequential", **kw))
+    monkeypatch.setenv("LP_HIST_OVERLAP", "1")
+    side = lp.run(lp.EngineConfig(mode="sequential", **kw))
+    tpp = lp.run(lp.EngineConfig(mode="tpp", **kw))
+    assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(inline.blocks, side.blocks))
+    assert all(a.values.tobytes() == b.values.tobytes() for a, b in zip(side.blocks, tpp.blocks))
+    clean = lp.run(lp.EngineConfig(mode="sequential", **dict(kw, history_sigma=0.0)))
+    assert any(a.values.tobytes() != b.values.tobytes() for a, b in zip(side.blocks, clean.blocks))
+
+
 def test_graph_replay_equals_eager_launches(monkeypatch):
     # the captured per-stage graphs (incl. the fork/join tail branch of a
     # forced pair split) replay exactly the eager launch sequence
