@@ -255,7 +255,7 @@ def roofline(prof, kern, n_tok, n_kv):
             kern[tag]["bytes_per_launch"] = b
             kern[tag]["gbs"] = b / (kern[tag]["avg_ms"] / 1e3) / 1e9
             kern[tag]["frac_of_hbm"] = kern[tag]["gbs"] / hbm
-    if "history_noise" in kern and os.environ.get("LP_HIST_OVERLAP", "1") != "0":
+    if "history_noise" in kern and os.environ.get("LP_HIST_OVERLAP", "0") == "1":
         kern["history_noise"]["note"] = ("side stream beside the GEMMs (lp_history_noise_co): the duration "
                                          "overlaps O-proj/FFN/QKV and is mostly off the critical path")
     if "attention" not in kern:

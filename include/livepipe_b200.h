@@ -360,9 +360,10 @@ LP_API int lp_history_noise(void* arena, int dtype, int d, const float* noise, i
 /* lp_history_noise (device counter-hash stream, bf16 arena) shaped to run on
    a side stream beside the tcgen05 GEMMs: two 128-thread CTAs per SM of
    <= 40 registers fit in what a GEMM CTA leaves free, so the corrupted-view
-   copy of layer l overlaps the previous layer's O-proj / FFN and this
-   layer's QKV instead of sitting on the critical path.  Same noise values
-   as lp_history_noise with noise == NULL.                                  */
+   copy of layer l can overlap the previous layer's O-proj / FFN and this
+   layer's QKV (runtime opt-in LP_HIST_OVERLAP=1; measured slower than the
+   in-line lp_history_noise at 14B).  Same noise values as lp_history_noise
+   with noise == NULL.                                                      */
 LP_API int lp_history_noise_co(void* arena, int d, int layer, int kv, const lp_block_desc* desc, int max_rows,
                                void* stream);
 

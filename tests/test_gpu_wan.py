@@ -299,9 +299,10 @@ def test_wan_tpp_long_stream_device_noise_equals_sequential(capacity):
 
 
 def test_history_noise_side_stream_equals_in_line(monkeypatch):
-    # device-RNG history noise on the low-priority side stream (lp_history_noise_co,
-    # forked after attention(l-1), joined before attention(l)) produces the
-    # same corrupted views as the in-line kernel: bitwise equal rollouts
+    # device-RNG history noise on the low-priority side stream (LP_HIST_OVERLAP=1:
+    # lp_history_noise_co, forked after attention(l-1), joined before
+    # attention(l)) produces the same corrupted views as the in-line kernel:
+    # bitwise equal rollouts
     _, pp = _profiles()
     kw = dict(profile=pp, precision="bf16", steps=4, cache_capacity=3, blocks=8, device_inputs=True,
               history_sigma=0.1, history_mode="fixed")
