@@ -243,3 +243,45 @@ def test_device_history_noise_streams_independent():
             c = float(torch.corrcoef(torch.stack([outs[i], outs[j]]))[0, 1])
             assert abs(c) < 0.015, (i, j, c)
             assert not torch.equal(outs[i], outs[j])
+
+
+def test_dynamic_item_queue_stress_bitwise_repeatable():
+    # the persistent kernel's items are claimed dynamically (global counter +
+    # a cluster-scope shared-memory ring per cluster pair): which cluster runs
+    # which item changes from launch to launch, the output must not.  30
+    # back-to-back launches on one stream (counter re-zeroed by the init
+    # kernel each time) and 10 more interleaved with a second workspace on a
+    # second stream, at the full 14B shape, all bitwise equal.
+    n_q, s_tok, heads = 4680, 1560, 40
+    d, rows = heads * 128, s_tok + 5 * n_q
+    g = torch.Generator(device=DEV).manual_seed(77)
+    karena = torch.randn((rows, d), generator=g, device=DEV).to(torch.bfloat16)
+    varena = torch.randn((rows, d), generator=g, device=DEV).to(torch.bfloat16)
+    q = torch.randn((n_q, d), generator=g, device=DEV).to(torch.bfloat16)
+    segs = [(0, s_tok)] + [(s_tok + n_q * s, n_q) for s in (3, 4, 0, 1)] + [(s_tok + 2 * n_q, n_q)]
+    desc = make_desc(9, segs, s_tok + 2 * n_q, n_q, 128, arena_order=1)
+    ddev = upload_desc(desc)
+    scale = float(np.float32(1.0) / np.float32(np.sqrt(128)))
+    n_kv = sum(n for _, n in segs)
+    streams = [torch.cuda.current_stream(), torch.cuda.Stream()]
+    wss = [_workspace(n_q, heads) for _ in streams]
+    outs = []
+
+    def launch(i, si):
+        out = torch.empty_like(q)
+        ws, nb = wss[si]
+        args = L.AttnArgs(L.LP_BF16, n_q, heads, 128, scale, q.data_ptr(), karena.data_ptr(), varena.data_ptr(),
+                          out.data_ptr(), ddev.data_ptr(), rows, n_kv, ws.data_ptr(), nb)
+        L.call("lp_attention", C.byref(args), streams[si].cuda_stream)
+        return out
+
+    for i in range(30):
+        outs.append(launch(i, 0))
+    streams[1].wait_stream(streams[0])
+    for i in range(10):
+        outs.append(launch(i, i % 2))
+    torch.cuda.synchronize()
+    ref = outs[0]
+    assert bool(torch.isfinite(ref.float()).all())
+    for o in outs[1:]:
+        assert torch.equal(o, ref)
